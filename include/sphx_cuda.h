@@ -1,0 +1,176 @@
+/*
+ * sphx_cuda.h -- the C ABI of the B200 (sm_100a) NNPS library (libsphx_cuda.so).
+ *
+ * This is the drop-in boundary for the reference's neighbour-search hot path.
+ * Plain C types only: pointers, sizes, a POD grid descriptor. No torch, no C++.
+ * Each entry point names the reference interface it replaces (paths relative to
+ * the reference's proj/ tree):
+ *
+ *   sphx_rcll            <- NeighborTable rcll(const RelCoords&, const CellGrid&,
+ *                                              Precision)           nnps.hpp:41, nnps.cpp:283-416
+ *   sphx_cell_link_list  <- NeighborTable cell_link_list(const ParticleSystem&,
+ *                                              const CellGrid&, Precision)
+ *                                                                   nnps.hpp:36, nnps.cpp:174-281
+ *   sphx_all_list        <- NeighborTable all_list(const ParticleSystem&, Precision)
+ *                                                                   nnps.hpp:31, nnps.cpp:128-172
+ *   sphx_rebin           <- void CellGrid::rebin(const ParticleSystem&)
+ *                                                                   cell_grid.hpp:147, cell_grid.cpp:66-108
+ *   sphx_build_rel_coords<- RelCoords build_rel_coords(const ParticleSystem&, CellGrid&)
+ *                                                                   cell_grid.hpp:181, cell_grid.cpp:114-133
+ *   sphx_rebuild_members <- void CellGrid::rebuild_members(const RelCoords&)
+ *                                                                   cell_grid.hpp:150, cell_grid.cpp:86-108
+ *   sphx_table_copy      <- (ownership hand-off of the returned NeighborTable, nnps.hpp:16-26)
+ *   sphx_last_error      <- the what() of the exception the reference would throw
+ *   (the reference's own C-style template is detail::range_f16_rel_2d & co,
+ *    detail/nnps_batch.hpp:13-41)
+ *
+ * Output contract (nnps.hpp:13-26): CSR with int64 offsets[n+1], int32 items,
+ * rows in original particle order, each row ascending, no self entries;
+ * bit-identical to the reference CPU implementation at the same precision.
+ *
+ * Error convention: every function returns SPHX_OK (0) or a negative code whose
+ * class mirrors the C++ exception the reference throws (the C++ shim rethrows the
+ * same type with sphx_last_error() as the message). There is no CPU fallback: a
+ * missing CUDA device or a device that is not sm_100 is SPHX_ERR_CUDA.
+ *
+ * Host-memory entry points are synchronous. *_device entry points take device
+ * pointers and are ordered on the context's stream (sphx_set_stream).
+ */
+#ifndef SPHX_CUDA_H
+#define SPHX_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPHX_OK 0
+#define SPHX_ERR_GENERIC (-1)          /* std::exception */
+#define SPHX_ERR_INVALID_ARGUMENT (-2) /* std::invalid_argument */
+#define SPHX_ERR_OUT_OF_RANGE (-3)     /* std::out_of_range */
+#define SPHX_ERR_RUNTIME (-4)          /* std::runtime_error */
+#define SPHX_ERR_CUDA (-5)             /* no usable sm_100 device / CUDA failure */
+#define SPHX_ERR_CAPACITY (-6)         /* device table capacity too small (device API) */
+
+/* Precision (binary16.hpp:87): arithmetic precision of the distance pipeline. */
+#define SPHX_FP64 0
+#define SPHX_FP32 1
+#define SPHX_FP16 2
+
+/* POD image of the CellGrid/Domain state the NNPS path consumes
+ * (cell_grid.hpp:55-96, domain.hpp:36-43). Axes >= dim are ignored. */
+typedef struct sphx_grid_desc {
+  int32_t dim;          /* 1..3 */
+  int32_t counts[3];    /* CellGrid::count(k) */
+  int32_t periodic[3];  /* CellGrid::periodic(k) */
+  int32_t reserved;
+  double hc[3];         /* CellGrid::hc(k): normalised cell edge 2*edge/h_d */
+  double origin[3];     /* CellGrid::origin_norm(k) */
+  double cutoff_norm;   /* CellGrid::cutoff_norm(): 2*radius/h_d */
+  double radius_phys;   /* CellGrid::radius_phys(): 2h */
+  double lo[3];         /* Domain::lo */
+  double hi[3];         /* Domain::hi */
+} sphx_grid_desc;
+
+/* Fill a descriptor exactly as CellGrid's constructor would (cell_grid.cpp:9-34).
+ * Returns SPHX_ERR_INVALID_ARGUMENT for radius <= 0 or a periodic axis with < 3 cells. */
+int sphx_grid_init(sphx_grid_desc* g, int32_t dim, const double lo[3], const double hi[3],
+                   double radius, const int32_t periodic[3]);
+
+typedef struct sphx_context sphx_context;
+
+/* Create a context on `device` (-1 = current). Fails with SPHX_ERR_CUDA when no
+ * sm_100 device is present. */
+int sphx_create(int device, sphx_context** out);
+void sphx_destroy(sphx_context* ctx);
+/* Message of the last error on this thread ("" if none). */
+const char* sphx_last_error(void);
+/* Use an external stream (a cudaStream_t, e.g. torch's current stream); NULL
+ * restores the context's own stream. */
+int sphx_set_stream(sphx_context* ctx, void* cuda_stream);
+/* Kernel launches issued by this context so far (diagnostics / bench). */
+int64_t sphx_launch_count(const sphx_context* ctx);
+
+/* ---------------- drop-in, host memory, synchronous ---------------- */
+
+/* rcll(rc, grid, prec). rel[k]/cell[k] are RelCoords::rel[k]/cell[k] (n entries,
+ * k < dim); items/cell_start are CellGrid::items() (n_items) and cell_start()
+ * (cell_total+1). On success *total = number of (directed) pairs; the table stays
+ * on the device until sphx_table_copy. */
+int sphx_rcll(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+              const double* const rel[3], const int32_t* const cell[3], int64_t n_items,
+              const int32_t* items, const int32_t* cell_start, int32_t precision,
+              int64_t* total);
+
+/* cell_link_list(ps, grid, prec). x[k] = ParticleSystem::x(k), h = ps.h(),
+ * cell_of[i] = CellGrid::cell_of(i). */
+int sphx_cell_link_list(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                        const double* const x[3], double h, int64_t n_items,
+                        const int32_t* items, const int32_t* cell_start,
+                        const int32_t* cell_of, int32_t precision, int64_t* total);
+
+/* all_list(ps, prec): O(N^2) reference backend. */
+int sphx_all_list(sphx_context* ctx, int32_t dim, int64_t n, const double* const x[3], double h,
+                  int32_t precision, int64_t* total);
+
+/* Copy the last table computed on this context to host buffers: offsets[n+1],
+ * items[total]. Either pointer may be NULL. */
+int sphx_table_copy(sphx_context* ctx, int64_t* offsets, int32_t* items);
+
+/* CellGrid::rebin(ps): cell_of[n], cell_start[cell_total+1], items[n]. A particle
+ * outside the grid -> SPHX_ERR_OUT_OF_RANGE "particle <i> lies outside the grid"
+ * (the lowest such index, as the reference's serial loop reports). */
+int sphx_rebin(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+               const double* const x[3], int32_t* cell_of, int32_t* cell_start, int32_t* items);
+
+/* build_rel_coords(ps, grid): rel[k][n], cell[k][n] plus the rebuilt membership. */
+int sphx_build_rel_coords(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                          const double* const x[3], double* const rel[3], int32_t* const cell[3],
+                          int32_t* cell_of, int32_t* cell_start, int32_t* items);
+
+/* CellGrid::rebuild_members(rc): membership from per-axis cells. */
+int sphx_rebuild_members(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                         const int32_t* const cell[3], int32_t* cell_of, int32_t* cell_start,
+                         int32_t* items);
+
+/* ---------------- device-resident, stream-ordered ---------------- */
+
+/* Same computation as sphx_rcll with every pointer in device memory. The table is
+ * written to d_offsets[n+1] / d_items[capacity]; d_offsets[n] always receives the
+ * exact total. If it exceeds `capacity`, items are not written and the call must
+ * be repeated with a larger buffer (the host can read d_offsets[n]).
+ * Does not synchronise. */
+int sphx_rcll_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                     const double* const d_rel[3], const int32_t* const d_cell[3],
+                     const int32_t* d_items, const int32_t* d_cell_start, int32_t precision,
+                     int64_t* d_offsets, int32_t* d_items_out, int64_t capacity);
+
+int sphx_cell_link_list_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                               const double* const d_x[3], double h, const int32_t* d_items,
+                               const int32_t* d_cell_start, const int32_t* d_cell_of,
+                               int32_t precision, int64_t* d_offsets, int32_t* d_items_out,
+                               int64_t capacity);
+
+/* Device binning + RCLL encoding: build_rel_coords on device pointers. Out-of-grid
+ * particles are not checked (the reference's build_rel_coords does not check). */
+int sphx_build_rel_coords_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                                 const double* const d_x[3], double* const d_rel[3],
+                                 int32_t* const d_cell[3], int32_t* d_cell_of,
+                                 int32_t* d_cell_start, int32_t* d_items);
+
+/* Device rebin; *d_bad receives the lowest out-of-grid particle index or -1. */
+int sphx_rebin_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                      const double* const d_x[3], int32_t* d_cell_of, int32_t* d_cell_start,
+                      int32_t* d_items, int64_t* d_bad);
+
+/* Per-kernel timing of the last sphx_*_device NNPS call when timing is enabled
+ * (CUDA events on the launching stream): encode and sweep in milliseconds. */
+int sphx_enable_timing(sphx_context* ctx, int on);
+int sphx_last_timing(sphx_context* ctx, float* encode_ms, float* sweep_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPHX_CUDA_H */

@@ -1,0 +1,267 @@
+"""ctypes binding of the C ABI (include/sphx_cuda.h) -> lib/libsphx_cuda.so.
+
+This is the Python-side view of the drop-in boundary. There is no CPU path:
+if the library or an sm_100 device is missing, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "lib", "libsphx_cuda.so")
+
+FP64, FP32, FP16 = 0, 1, 2
+PRECISIONS = {"fp64": FP64, "fp32": FP32, "fp16": FP16}
+
+OK = 0
+ERR_GENERIC, ERR_INVALID_ARGUMENT, ERR_OUT_OF_RANGE = -1, -2, -3
+ERR_RUNTIME, ERR_CUDA, ERR_CAPACITY = -4, -5, -6
+
+
+class SphxCudaError(RuntimeError):
+    """CUDA / device failure (SPHX_ERR_CUDA)."""
+
+
+class GridDesc(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("counts", C.c_int32 * 3), ("periodic", C.c_int32 * 3),
+                ("reserved", C.c_int32), ("hc", C.c_double * 3), ("origin", C.c_double * 3),
+                ("cutoff_norm", C.c_double), ("radius_phys", C.c_double),
+                ("lo", C.c_double * 3), ("hi", C.c_double * 3)]
+
+    @property
+    def cell_total(self) -> int:
+        t = 1
+        for k in range(self.dim):
+            t *= self.counts[k]
+        return t
+
+    def as_dict(self) -> dict:
+        return {"dim": self.dim, "counts": list(self.counts), "periodic": list(self.periodic),
+                "hc": list(self.hc), "origin": list(self.origin), "cutoff_norm": self.cutoff_norm,
+                "radius_phys": self.radius_phys, "lo": list(self.lo), "hi": list(self.hi)}
+
+
+_lib = None
+
+
+def lib():
+    """Load libsphx_cuda.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                          "(the NNPS path has no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    p3 = C.c_void_p * 3
+    G = C.POINTER(GridDesc)
+    sigs = {
+        "sphx_last_error": (C.c_char_p, []),
+        "sphx_grid_init": (C.c_int, [G, i32, C.POINTER(dbl), C.POINTER(dbl), dbl, C.POINTER(i32)]),
+        "sphx_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
+        "sphx_destroy": (None, [vp]),
+        "sphx_set_stream": (C.c_int, [vp, vp]),
+        "sphx_launch_count": (i64, [vp]),
+        "sphx_rcll": (C.c_int, [vp, G, i64, p3, p3, i64, vp, vp, i32, C.POINTER(i64)]),
+        "sphx_cell_link_list": (C.c_int, [vp, G, i64, p3, dbl, i64, vp, vp, vp, i32,
+                                          C.POINTER(i64)]),
+        "sphx_all_list": (C.c_int, [vp, i32, i64, p3, dbl, i32, C.POINTER(i64)]),
+        "sphx_table_copy": (C.c_int, [vp, vp, vp]),
+        "sphx_rebin": (C.c_int, [vp, G, i64, p3, vp, vp, vp]),
+        "sphx_build_rel_coords": (C.c_int, [vp, G, i64, p3, p3, p3, vp, vp, vp]),
+        "sphx_rebuild_members": (C.c_int, [vp, G, i64, p3, vp, vp, vp]),
+        "sphx_rcll_device": (C.c_int, [vp, G, i64, p3, p3, vp, vp, i32, vp, vp, i64]),
+        "sphx_cell_link_list_device": (C.c_int, [vp, G, i64, p3, dbl, vp, vp, vp, i32, vp, vp,
+                                                 i64]),
+        "sphx_build_rel_coords_device": (C.c_int, [vp, G, i64, p3, p3, p3, vp, vp, vp]),
+        "sphx_rebin_device": (C.c_int, [vp, G, i64, p3, vp, vp, vp, vp]),
+        "sphx_enable_timing": (C.c_int, [vp, C.c_int]),
+        "sphx_last_timing": (C.c_int, [vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+    }
+    for name, (res, args) in sigs.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+EXPORTED = ("sphx_last_error", "sphx_grid_init", "sphx_create", "sphx_destroy",
+            "sphx_set_stream", "sphx_launch_count", "sphx_rcll", "sphx_cell_link_list",
+            "sphx_all_list", "sphx_table_copy", "sphx_rebin", "sphx_build_rel_coords",
+            "sphx_rebuild_members", "sphx_rcll_device", "sphx_cell_link_list_device",
+            "sphx_build_rel_coords_device", "sphx_rebin_device", "sphx_enable_timing",
+            "sphx_last_timing")
+
+
+def check(rc: int) -> None:
+    """Map a C-ABI status to the exception class the reference throws."""
+    if rc == OK:
+        return
+    msg = lib().sphx_last_error().decode()
+    if rc == ERR_INVALID_ARGUMENT:
+        raise ValueError(msg)          # std::invalid_argument
+    if rc == ERR_OUT_OF_RANGE:
+        raise IndexError(msg)          # std::out_of_range
+    if rc == ERR_CUDA:
+        raise SphxCudaError(msg)
+    raise RuntimeError(msg)            # std::runtime_error / generic
+
+
+def _d3(v) -> "C.Array":
+    v = list(v) + [0.0] * (3 - len(v))
+    return (C.c_double * 3)(*[float(a) for a in v])
+
+
+def grid_init(dim: int, lo, hi, radius: float, periodic=(0, 0, 0)) -> GridDesc:
+    """CellGrid(Domain::box(dim, lo, hi), radius, periodic) as a descriptor."""
+    g = GridDesc()
+    p = (C.c_int32 * 3)(*[int(bool(x)) for x in list(periodic) + [0] * (3 - len(periodic))])
+    check(lib().sphx_grid_init(C.byref(g), dim, _d3(lo), _d3(hi), float(radius), p))
+    return g
+
+
+def _ptr3(arrs):
+    ptrs = [a.ctypes.data if a is not None else None for a in arrs] + [None] * (3 - len(arrs))
+    return (C.c_void_p * 3)(*ptrs)
+
+
+def _dptr3(tensors):
+    ptrs = [t.data_ptr() if t is not None else None for t in tensors]
+    ptrs += [None] * (3 - len(ptrs))
+    return (C.c_void_p * 3)(*ptrs)
+
+
+def _c64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _c32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+class Context:
+    """One sphx_context: a CUDA stream plus grow-only device buffers."""
+
+    def __init__(self, device: int = -1):
+        h = C.c_void_p()
+        check(lib().sphx_create(device, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().sphx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launches(self) -> int:
+        return int(lib().sphx_launch_count(self.h))
+
+    def set_stream(self, stream_handle: int | None):
+        check(lib().sphx_set_stream(self.h, stream_handle))
+
+    def enable_timing(self, on: bool = True):
+        check(lib().sphx_enable_timing(self.h, int(on)))
+
+    def last_timing(self):
+        e, s = C.c_float(), C.c_float()
+        check(lib().sphx_last_timing(self.h, C.byref(e), C.byref(s)))
+        return e.value, s.value
+
+    # ---- drop-in host API -------------------------------------------------------------
+    def _fetch(self, n: int, total: int):
+        off = np.empty(n + 1, np.int64)
+        items = np.empty(max(total, 1), np.int32)
+        check(lib().sphx_table_copy(self.h, off.ctypes.data, items.ctypes.data))
+        return off, items[:total]
+
+    def rcll(self, grid: GridDesc, rel, cell, items, cell_start, prec: int):
+        rel = [_c64(a) for a in rel]
+        cell = [_c32(a) for a in cell]
+        items = _c32(items)
+        cell_start = _c32(cell_start)
+        n = len(rel[0]) if rel else 0
+        tot = C.c_int64()
+        check(lib().sphx_rcll(self.h, C.byref(grid), n, _ptr3(rel), _ptr3(cell), len(items),
+                              items.ctypes.data, cell_start.ctypes.data, prec, C.byref(tot)))
+        return self._fetch(n, tot.value)
+
+    def cell_link_list(self, grid: GridDesc, x, h: float, items, cell_start, cell_of, prec: int):
+        x = [_c64(a) for a in x]
+        items, cell_start, cell_of = _c32(items), _c32(cell_start), _c32(cell_of)
+        n = len(x[0])
+        tot = C.c_int64()
+        check(lib().sphx_cell_link_list(self.h, C.byref(grid), n, _ptr3(x), float(h), len(items),
+                                        items.ctypes.data, cell_start.ctypes.data,
+                                        cell_of.ctypes.data, prec, C.byref(tot)))
+        return self._fetch(n, tot.value)
+
+    def all_list(self, x, h: float, prec: int):
+        x = [_c64(a) for a in x]
+        n = len(x[0])
+        tot = C.c_int64()
+        check(lib().sphx_all_list(self.h, len(x), n, _ptr3(x), float(h), prec, C.byref(tot)))
+        return self._fetch(n, tot.value)
+
+    def rebin(self, grid: GridDesc, x):
+        x = [_c64(a) for a in x]
+        n = len(x[0])
+        cell_of = np.empty(max(n, 1), np.int32)
+        start = np.empty(grid.cell_total + 1, np.int32)
+        items = np.empty(max(n, 1), np.int32)
+        check(lib().sphx_rebin(self.h, C.byref(grid), n, _ptr3(x), cell_of.ctypes.data,
+                               start.ctypes.data, items.ctypes.data))
+        return cell_of[:n], start, items[:n]
+
+    def build_rel_coords(self, grid: GridDesc, x):
+        x = [_c64(a) for a in x]
+        n = len(x[0])
+        d = grid.dim
+        rel = [np.empty(max(n, 1), np.float64) for _ in range(d)]
+        cell = [np.empty(max(n, 1), np.int32) for _ in range(d)]
+        cell_of = np.empty(max(n, 1), np.int32)
+        start = np.empty(grid.cell_total + 1, np.int32)
+        items = np.empty(max(n, 1), np.int32)
+        check(lib().sphx_build_rel_coords(self.h, C.byref(grid), n, _ptr3(x), _ptr3(rel),
+                                          _ptr3(cell), cell_of.ctypes.data, start.ctypes.data,
+                                          items.ctypes.data))
+        return [r[:n] for r in rel], [c[:n] for c in cell], cell_of[:n], start, items[:n]
+
+    def rebuild_members(self, grid: GridDesc, cell):
+        cell = [_c32(a) for a in cell]
+        n = len(cell[0])
+        cell_of = np.empty(max(n, 1), np.int32)
+        start = np.empty(grid.cell_total + 1, np.int32)
+        items = np.empty(max(n, 1), np.int32)
+        check(lib().sphx_rebuild_members(self.h, C.byref(grid), n, _ptr3(cell),
+                                         cell_of.ctypes.data, start.ctypes.data,
+                                         items.ctypes.data))
+        return cell_of[:n], start, items[:n]
+
+    # ---- device-resident API (torch tensors as device memory) ---------------------------
+    def rcll_device(self, grid, rel, cell, items, cell_start, prec, offsets, items_out):
+        check(lib().sphx_rcll_device(self.h, C.byref(grid), rel[0].numel(), _dptr3(rel),
+                                     _dptr3(cell), items.data_ptr(), cell_start.data_ptr(), prec,
+                                     offsets.data_ptr(), items_out.data_ptr(), items_out.numel()))
+
+    def cell_link_list_device(self, grid, x, h, items, cell_start, cell_of, prec, offsets,
+                              items_out):
+        check(lib().sphx_cell_link_list_device(self.h, C.byref(grid), x[0].numel(), _dptr3(x),
+                                               float(h), items.data_ptr(), cell_start.data_ptr(),
+                                               cell_of.data_ptr(), prec, offsets.data_ptr(),
+                                               items_out.data_ptr(), items_out.numel()))
+
+    def build_rel_coords_device(self, grid, x, rel, cell, cell_of, cell_start, items):
+        check(lib().sphx_build_rel_coords_device(self.h, C.byref(grid), x[0].numel(), _dptr3(x),
+                                                 _dptr3(rel), _dptr3(cell), cell_of.data_ptr(),
+                                                 cell_start.data_ptr(), items.data_ptr()))

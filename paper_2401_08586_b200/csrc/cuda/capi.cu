@@ -1,0 +1,718 @@
+// C ABI of libsphx_cuda.so (include/sphx_cuda.h): context, device buffers,
+// precision constants, and the host/device entry points of the NNPS path.
+// No CPU fallback anywhere: every neighbour decision is made on the device.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "sphx/binary16.hpp"
+#include "sphx_cuda.h"
+
+namespace sphx_dev {
+// sweep.cu
+void launch_encode(int dim, int prec, int n, const double* const x[3], const int32_t* items,
+                   void* own, void* pos_s, unsigned long long* tiles, int ntiles, int* counter,
+                   cudaStream_t st);
+void launch_sweep(int dim, int prec, int mode, const SweepArgs& a, cudaStream_t st);
+size_t coord_bytes(int dim, int prec);
+int sweep_block_threads(int dim);
+// binning.cu
+int64_t scan_tiles(int64_t C);
+void launch_locate(int mode, const LocateArgs& a, cudaStream_t st);
+void launch_scan_counts(const int32_t* in, int32_t* out, int64_t C, unsigned long long* tiles,
+                        int* counter, cudaStream_t st);
+void launch_scatter_sort(int n, int64_t C, const int32_t* cell_of, const int32_t* slot,
+                         const int32_t* start, int32_t* items, cudaStream_t st);
+}  // namespace sphx_dev
+
+using namespace sphx_dev;
+
+// ----------------------------------------------------------------------------------
+// errors
+// ----------------------------------------------------------------------------------
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e__ = (call);                                                             \
+    if (e__ != cudaSuccess)                                                               \
+      return fail(SPHX_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e__));    \
+  } while (0)
+
+#define CKL()                                                                             \
+  do {                                                                                    \
+    cudaError_t e__ = cudaGetLastError();                                                 \
+    if (e__ != cudaSuccess)                                                               \
+      return fail(SPHX_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e__)); \
+  } while (0)
+
+#define TRY(x)              \
+  do {                      \
+    int r__ = (x);          \
+    if (r__ != SPHX_OK) return r__; \
+  } while (0)
+
+// ----------------------------------------------------------------------------------
+// device buffers (grow-only)
+// ----------------------------------------------------------------------------------
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t need) {
+    if (need <= bytes) return SPHX_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    size_t want = std::max<size_t>(need, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      return fail(SPHX_ERR_CUDA, std::string("cudaMalloc(") + std::to_string(want) +
+                                     "): " + cudaGetErrorString(e));
+    }
+    bytes = want;
+    return SPHX_OK;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+}  // namespace
+
+struct sphx_context {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  bool timing = false;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  float t_encode = 0.f, t_sweep = 0.f;
+  // inputs staged from host
+  Buf in_x[3], in_cell[3], in_items, in_start, in_cellof;
+  // encode / sweep scratch
+  Buf pos_own, pos_s, tiles, counter;
+  // table of the last host-API call
+  Buf t_offsets, t_items;
+  int64_t t_n = -1, t_total = 0, t_capacity = 0;
+  // binning scratch
+  Buf b_counts, b_slot, b_bad, b_tiles, b_out_cellof, b_out_start, b_out_items, b_rel[3], b_cell[3];
+};
+
+namespace {
+
+// ----------------------------------------------------------------------------------
+// precision constants (host, exact)
+// ----------------------------------------------------------------------------------
+double r16(double x) { return sphx::round16(x); }
+uint16_t b16(double x) { return sphx::Binary16::encode(x); }
+
+uint16_t thr16(double cutoff16) {
+  // smallest binary16 a >= 0 with round16(sqrt(a)) >= cutoff16 (nnps.cpp:344, :409);
+  // the predicate is monotone in a, so bisect over the finite patterns + inf.
+  if (std::isnan(cutoff16)) return 0;
+  auto pred = [&](uint32_t b) {
+    return r16(std::sqrt(sphx::Binary16::decode((uint16_t)b))) >= cutoff16;
+  };
+  if (pred(0)) return 0;
+  uint32_t lo = 0, hi = 0x7C00u;  // pred(inf) holds
+  while (hi - lo > 1) {
+    const uint32_t mid = lo + (hi - lo) / 2;
+    (pred(mid) ? hi : lo) = mid;
+  }
+  return (uint16_t)hi;
+}
+
+float thr32(float cutoff) {
+  if (std::isnan(cutoff)) return 0.0f;
+  uint32_t lo = 0, hi = 0x7F800000u;  // predicate true at +inf
+  auto pred = [&](uint32_t b) {
+    float a;
+    std::memcpy(&a, &b, 4);
+    return std::sqrt(a) >= cutoff;
+  };
+  if (pred(lo)) return 0.0f;
+  while (hi - lo > 1) {
+    const uint32_t mid = lo + (hi - lo) / 2;
+    (pred(mid) ? hi : lo) = mid;
+  }
+  float t;
+  std::memcpy(&t, &hi, 4);
+  return t;
+}
+
+double thr64(double cutoff) {
+  if (std::isnan(cutoff)) return 0.0;
+  uint64_t lo = 0, hi = 0x7FF0000000000000ull;
+  auto pred = [&](uint64_t b) {
+    double a;
+    std::memcpy(&a, &b, 8);
+    return std::sqrt(a) >= cutoff;
+  };
+  if (pred(lo)) return 0.0;
+  while (hi - lo > 1) {
+    const uint64_t mid = lo + (hi - lo) / 2;
+    (pred(mid) ? hi : lo) = mid;
+  }
+  double t;
+  std::memcpy(&t, &hi, 8);
+  return t;
+}
+
+double span_of(const sphx_grid_desc& g, int k) { return g.hi[k] - g.lo[k]; }
+
+// mode RCLL: cutoff = round_to(prec, cutoff_norm), hh/cc from hc (nnps.cpp:289-295)
+// mode CLL/ALL: cutoff = round_to(prec, 2h), shifts = round_to(prec, span) (:177-197)
+PrecConsts make_consts(int mode, int prec, const sphx_grid_desc& g, double h) {
+  PrecConsts c;
+  std::memset(&c, 0, sizeof(c));
+  const double cut = mode == MODE_RCLL ? g.cutoff_norm : 2.0 * h;
+  for (int k = 0; k < 3; ++k) {
+    const double hc = k < g.dim ? g.hc[k] : 0.0;
+    const double sp = k < g.dim ? span_of(g, k) : 0.0;
+    c.h_hh[k] = b16(0.5 * hc);
+    c.h_cc[k] = b16(hc);
+    c.h_sh[k] = b16(sp);
+    c.f_hh[k] = (float)(0.5 * hc);
+    c.f_cc[k] = (float)hc;
+    c.f_sh[k] = (float)sp;
+    c.d_hh[k] = 0.5 * hc;
+    c.d_cc[k] = hc;
+    c.d_sh[k] = sp;
+  }
+  c.h_thr = thr16(r16(cut));
+  c.f_thr = thr32((float)cut);
+  c.d_thr = thr64(cut);
+  return c;
+}
+
+int check_prec_dim(int32_t prec, int32_t dim) {
+  if (prec < SPHX_FP64 || prec > SPHX_FP16) return fail(SPHX_ERR_INVALID_ARGUMENT, "unknown precision");
+  if (dim < 1 || dim > 3) return fail(SPHX_ERR_INVALID_ARGUMENT, "domain dimension must be 1, 2 or 3");
+  return SPHX_OK;
+}
+
+int64_t cell_total(const sphx_grid_desc& g) {
+  int64_t t = 1;
+  for (int k = 0; k < g.dim; ++k) t *= g.counts[k];
+  return t;
+}
+
+GridConsts grid_consts(const sphx_grid_desc& g) {
+  GridConsts gc;
+  gc.dim = g.dim;
+  for (int k = 0; k < 3; ++k) {
+    gc.counts[k] = k < g.dim ? g.counts[k] : 1;
+    gc.wrap[k] = (k < g.dim && g.periodic[k] && g.counts[k] > 2) ? 1 : 0;
+  }
+  return gc;
+}
+
+BinConsts bin_consts(const sphx_grid_desc& g) {
+  BinConsts b;
+  std::memset(&b, 0, sizeof(b));
+  b.dim = g.dim;
+  double hd = 0.0;
+  for (int k = 0; k < g.dim; ++k) hd = std::max(hd, span_of(g, k));  // Domain::h_d
+  b.hd = hd;
+  for (int k = 0; k < 3; ++k) {
+    b.counts[k] = k < g.dim ? g.counts[k] : 1;
+    b.hc[k] = g.hc[k];
+    b.origin[k] = g.origin[k];
+    b.lo[k] = g.lo[k];
+    b.hi[k] = g.hi[k];
+  }
+  return b;
+}
+
+int upload(sphx_context* ctx, Buf& b, const void* src, size_t bytes) {
+  TRY(b.ensure(bytes));
+  if (bytes) CK(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return SPHX_OK;
+}
+
+// Encode + sweep on device pointers. src = rel (RCLL) or positions (CLL/ALL).
+int run_nnps(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n64,
+             const double* const src[3], const int32_t* const cellk[3], const int32_t* items,
+             const int32_t* start, const int32_t* cell_of, int prec, double h, int64_t* d_off,
+             int32_t* d_items, int64_t capacity, bool encode) {
+  if (n64 > INT32_MAX - 1024) return fail(SPHX_ERR_INVALID_ARGUMENT, "too many particles for int32 ids");
+  const int n = (int)n64;
+  cudaStream_t st = ctx->stream;
+  if (n == 0) {
+    CK(cudaMemsetAsync(d_off, 0, sizeof(int64_t), st));
+    return SPHX_OK;
+  }
+  const size_t cb = coord_bytes(g.dim, prec);
+  const int bt = sweep_block_threads(g.dim);
+  const int nblocks = (n + bt - 1) / bt;
+  TRY(ctx->pos_own.ensure(cb * n));
+  if (mode != MODE_ALL) TRY(ctx->pos_s.ensure(cb * n));
+  TRY(ctx->tiles.ensure(sizeof(unsigned long long) * nblocks));
+  TRY(ctx->counter.ensure(sizeof(int)));
+
+  if (ctx->timing) CK(cudaEventRecord(ctx->ev[0], st));
+  if (encode) {
+    launch_encode(g.dim, prec, n, src, mode == MODE_ALL ? nullptr : items, ctx->pos_own.p,
+                  ctx->pos_s.p, ctx->tiles.as<unsigned long long>(), nblocks,
+                  ctx->counter.as<int>(), st);
+    CKL();
+    ++ctx->launches;
+  } else {
+    CK(cudaMemsetAsync(ctx->tiles.p, 0, sizeof(unsigned long long) * nblocks, st));
+    CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), st));
+  }
+  if (ctx->timing) CK(cudaEventRecord(ctx->ev[1], st));
+
+  SweepArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.n = n;
+  a.g = grid_consts(g);
+  a.c = make_consts(mode, prec, g, h);
+  a.cell_start = start;
+  a.pid_s = items;
+  a.pos_own = ctx->pos_own.p;
+  a.pos_s = mode == MODE_ALL ? ctx->pos_own.p : ctx->pos_s.p;
+  for (int k = 0; k < 3; ++k) a.cellk[k] = cellk ? cellk[k] : nullptr;
+  a.cell_of = cell_of;
+  a.offsets = d_off;
+  a.items = d_items;
+  a.capacity = capacity;
+  a.tiles = ctx->tiles.as<unsigned long long>();
+  a.block_counter = ctx->counter.as<int>();
+  launch_sweep(g.dim, prec, mode, a, st);
+  CKL();
+  ++ctx->launches;
+  if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], st));
+  return SPHX_OK;
+}
+
+// Host-API driver: stage, run, read the total, grow + re-run when needed.
+int run_host_table(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n,
+                   const double* const d_src[3], const int32_t* const d_cellk[3],
+                   const int32_t* d_items, const int32_t* d_start, const int32_t* d_cellof,
+                   int prec, double h, int64_t* total) {
+  TRY(ctx->t_offsets.ensure(sizeof(int64_t) * (n + 1)));
+  if (ctx->t_capacity < 1) {
+    const int64_t guess = n * (g.dim == 3 ? 80 : (g.dim == 2 ? 24 : 8));
+    ctx->t_capacity = std::max<int64_t>(guess, 1 << 16);
+  }
+  TRY(ctx->t_items.ensure(sizeof(int32_t) * ctx->t_capacity));
+  bool encode = true;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    TRY(run_nnps(ctx, mode, g, n, d_src, d_cellk, d_items, d_start, d_cellof, prec, h,
+                 ctx->t_offsets.as<int64_t>(), ctx->t_items.as<int32_t>(), ctx->t_capacity,
+                 encode));
+    int64_t tot = 0;
+    CK(cudaMemcpyAsync(&tot, ctx->t_offsets.as<int64_t>() + n, sizeof(int64_t),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (tot <= ctx->t_capacity) {
+      ctx->t_n = n;
+      ctx->t_total = tot;
+      *total = tot;
+      if (ctx->timing) {
+        cudaEventElapsedTime(&ctx->t_encode, ctx->ev[0], ctx->ev[1]);
+        cudaEventElapsedTime(&ctx->t_sweep, ctx->ev[1], ctx->ev[2]);
+      }
+      return SPHX_OK;
+    }
+    ctx->t_capacity = tot + tot / 8 + 1024;
+    TRY(ctx->t_items.ensure(sizeof(int32_t) * ctx->t_capacity));
+    encode = false;
+  }
+  return fail(SPHX_ERR_RUNTIME, "neighbour table did not fit after regrowth");
+}
+
+int check_ctx(sphx_context* ctx) {
+  if (!ctx) return fail(SPHX_ERR_INVALID_ARGUMENT, "null context");
+  CK(cudaSetDevice(ctx->device));
+  return SPHX_OK;
+}
+
+// Binning on device pointers (locate -> counts -> scan -> scatter -> per-cell sort).
+int run_binning(sphx_context* ctx, int bmode, const sphx_grid_desc& g, int64_t n64,
+                const double* const d_x[3], const int32_t* const d_cell_in[3],
+                double* const d_rel[3], int32_t* const d_cell[3], int32_t* d_cell_of,
+                int32_t* d_start, int32_t* d_items, unsigned long long* d_bad) {
+  const int n = (int)n64;
+  const int64_t C = cell_total(g);
+  cudaStream_t st = ctx->stream;
+  TRY(ctx->b_counts.ensure(sizeof(int32_t) * std::max<int64_t>(C, 1)));
+  TRY(ctx->b_slot.ensure(sizeof(int32_t) * std::max(n, 1)));
+  const int64_t nt = std::max<int64_t>(scan_tiles(C), 1);
+  TRY(ctx->b_tiles.ensure(sizeof(unsigned long long) * nt + 16));
+  CK(cudaMemsetAsync(ctx->b_counts.p, 0, sizeof(int32_t) * C, st));
+  CK(cudaMemsetAsync(ctx->b_tiles.p, 0, sizeof(unsigned long long) * nt + 16, st));
+  LocateArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.n = n;
+  a.g = bin_consts(g);
+  for (int k = 0; k < 3; ++k) {
+    a.x[k] = d_x ? d_x[k] : nullptr;
+    a.cell_in[k] = d_cell_in ? d_cell_in[k] : nullptr;
+    a.rel_out[k] = d_rel ? d_rel[k] : nullptr;
+    a.cell_out[k] = d_cell ? d_cell[k] : nullptr;
+  }
+  a.cell_of = d_cell_of;
+  a.counts = ctx->b_counts.as<int32_t>();
+  a.slot = ctx->b_slot.as<int32_t>();
+  a.bad = d_bad;
+  launch_locate(bmode, a, st);
+  CKL();
+  ++ctx->launches;
+  unsigned long long* tiles = ctx->b_tiles.as<unsigned long long>();
+  launch_scan_counts(a.counts, d_start, C, tiles, reinterpret_cast<int*>(tiles + nt), st);
+  CKL();
+  ++ctx->launches;
+  launch_scatter_sort(n, C, d_cell_of, a.slot, d_start, d_items, st);
+  CKL();
+  ctx->launches += 2;
+  return SPHX_OK;
+}
+
+}  // namespace
+
+// ==================================================================================
+// C ABI
+// ==================================================================================
+extern "C" {
+
+const char* sphx_last_error(void) { return g_err.c_str(); }
+
+int sphx_grid_init(sphx_grid_desc* g, int32_t dim, const double lo[3], const double hi[3],
+                   double radius, const int32_t periodic[3]) {
+  // CellGrid::CellGrid (cell_grid.cpp:9-34) and Domain::validate (domain.hpp:29-34)
+  if (!g) return fail(SPHX_ERR_INVALID_ARGUMENT, "null grid");
+  std::memset(g, 0, sizeof(*g));
+  if (dim < 1 || dim > 3) return fail(SPHX_ERR_INVALID_ARGUMENT, "domain dimension must be 1, 2 or 3");
+  for (int k = 0; k < dim; ++k)
+    if (!(lo[k] < hi[k])) return fail(SPHX_ERR_INVALID_ARGUMENT, "domain bounds must satisfy lo < hi");
+  if (!(radius > 0.0)) return fail(SPHX_ERR_INVALID_ARGUMENT, "search radius must be positive");
+  g->dim = dim;
+  double hd = 0.0;
+  for (int k = 0; k < dim; ++k) hd = std::max(hd, hi[k] - lo[k]);
+  g->cutoff_norm = 2.0 * radius / hd;
+  g->radius_phys = radius;
+  for (int k = 0; k < 3; ++k) {
+    g->counts[k] = 1;
+    g->lo[k] = lo[k];
+    g->hi[k] = hi[k];
+    g->periodic[k] = periodic ? (periodic[k] != 0) : 0;
+  }
+  for (int k = 0; k < dim; ++k) {
+    const double span = hi[k] - lo[k];
+    double edge;
+    if (g->periodic[k]) {
+      const int c = static_cast<int>(std::floor(span / radius + 1e-12));
+      g->counts[k] = c > 0 ? c : 1;
+      edge = span / g->counts[k];
+      if (g->counts[k] < 3) return fail(SPHX_ERR_INVALID_ARGUMENT, "periodic axis needs at least 3 cells");
+    } else {
+      g->counts[k] = static_cast<int>(std::ceil(span / radius - 1e-12));
+      if (g->counts[k] < 1) g->counts[k] = 1;
+      edge = radius;
+    }
+    g->hc[k] = 2.0 * edge / hd;
+    g->origin[k] = (2.0 * lo[k] - (hi[k] + lo[k])) / hd;
+  }
+  return SPHX_OK;
+}
+
+int sphx_create(int device, sphx_context** out) {
+  if (!out) return fail(SPHX_ERR_INVALID_ARGUMENT, "null output");
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(SPHX_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  if (device < 0) CK(cudaGetDevice(&device));
+  if (device >= ndev) return fail(SPHX_ERR_CUDA, "device index out of range");
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(SPHX_ERR_CUDA, std::string("libsphx_cuda is built for sm_100a (B200); device is ") +
+                                   prop.name + " sm_" + std::to_string(prop.major) +
+                                   std::to_string(prop.minor));
+  CK(cudaSetDevice(device));
+  auto* ctx = new sphx_context();
+  ctx->device = device;
+  e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return fail(SPHX_ERR_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+  }
+  ctx->stream = ctx->own_stream;
+  for (auto& ev : ctx->ev) cudaEventCreate(&ev);
+  *out = ctx;
+  return SPHX_OK;
+}
+
+void sphx_destroy(sphx_context* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  Buf* all[] = {&ctx->in_x[0], &ctx->in_x[1], &ctx->in_x[2], &ctx->in_cell[0], &ctx->in_cell[1],
+                &ctx->in_cell[2], &ctx->in_items, &ctx->in_start, &ctx->in_cellof, &ctx->pos_own,
+                &ctx->pos_s, &ctx->tiles, &ctx->counter, &ctx->t_offsets, &ctx->t_items,
+                &ctx->b_counts, &ctx->b_slot, &ctx->b_bad, &ctx->b_tiles, &ctx->b_out_cellof,
+                &ctx->b_out_start, &ctx->b_out_items, &ctx->b_rel[0], &ctx->b_rel[1],
+                &ctx->b_rel[2], &ctx->b_cell[0], &ctx->b_cell[1], &ctx->b_cell[2]};
+  for (Buf* b : all) b->release();
+  for (auto& ev : ctx->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+
+int sphx_set_stream(sphx_context* ctx, void* stream) {
+  TRY(check_ctx(ctx));
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  return SPHX_OK;
+}
+
+int64_t sphx_launch_count(const sphx_context* ctx) { return ctx ? ctx->launches : 0; }
+
+int sphx_enable_timing(sphx_context* ctx, int on) {
+  TRY(check_ctx(ctx));
+  ctx->timing = on != 0;
+  return SPHX_OK;
+}
+
+int sphx_last_timing(sphx_context* ctx, float* encode_ms, float* sweep_ms) {
+  TRY(check_ctx(ctx));
+  if (!ctx->timing) return fail(SPHX_ERR_INVALID_ARGUMENT, "timing not enabled");
+  CK(cudaEventSynchronize(ctx->ev[2]));
+  float e = 0.f, s = 0.f;
+  CK(cudaEventElapsedTime(&e, ctx->ev[0], ctx->ev[1]));
+  CK(cudaEventElapsedTime(&s, ctx->ev[1], ctx->ev[2]));
+  if (encode_ms) *encode_ms = e;
+  if (sweep_ms) *sweep_ms = s;
+  return SPHX_OK;
+}
+
+// ---------------- drop-in host API ----------------
+
+int sphx_rcll(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+              const double* const rel[3], const int32_t* const cell[3], int64_t n_items,
+              const int32_t* items, const int32_t* cell_start, int32_t precision,
+              int64_t* total) {
+  TRY(check_ctx(ctx));
+  if (!grid || !total) return fail(SPHX_ERR_INVALID_ARGUMENT, "null argument");
+  TRY(check_prec_dim(precision, grid->dim));
+  if (n_items != n) return fail(SPHX_ERR_INVALID_ARGUMENT, "grid membership is stale");  // nnps.cpp:298
+  const int64_t C = cell_total(*grid);
+  const double* d_rel[3] = {nullptr, nullptr, nullptr};
+  const int32_t* d_cell[3] = {nullptr, nullptr, nullptr};
+  for (int k = 0; k < grid->dim; ++k) {
+    TRY(upload(ctx, ctx->in_x[k], rel[k], sizeof(double) * n));
+    TRY(upload(ctx, ctx->in_cell[k], cell[k], sizeof(int32_t) * n));
+    d_rel[k] = ctx->in_x[k].as<double>();
+    d_cell[k] = ctx->in_cell[k].as<int32_t>();
+  }
+  TRY(upload(ctx, ctx->in_items, items, sizeof(int32_t) * n));
+  TRY(upload(ctx, ctx->in_start, cell_start, sizeof(int32_t) * (C + 1)));
+  return run_host_table(ctx, MODE_RCLL, *grid, n, d_rel, d_cell, ctx->in_items.as<int32_t>(),
+                        ctx->in_start.as<int32_t>(), nullptr, precision, 0.0, total);
+}
+
+int sphx_cell_link_list(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                        const double* const x[3], double h, int64_t n_items,
+                        const int32_t* items, const int32_t* cell_start,
+                        const int32_t* cell_of, int32_t precision, int64_t* total) {
+  TRY(check_ctx(ctx));
+  if (!grid || !total) return fail(SPHX_ERR_INVALID_ARGUMENT, "null argument");
+  TRY(check_prec_dim(precision, grid->dim));
+  if (n_items != n)
+    return fail(SPHX_ERR_INVALID_ARGUMENT, "grid membership is stale; rebin first");  // nnps.cpp:184
+  const int64_t C = cell_total(*grid);
+  const double* d_x[3] = {nullptr, nullptr, nullptr};
+  for (int k = 0; k < grid->dim; ++k) {
+    TRY(upload(ctx, ctx->in_x[k], x[k], sizeof(double) * n));
+    d_x[k] = ctx->in_x[k].as<double>();
+  }
+  TRY(upload(ctx, ctx->in_items, items, sizeof(int32_t) * n));
+  TRY(upload(ctx, ctx->in_start, cell_start, sizeof(int32_t) * (C + 1)));
+  TRY(upload(ctx, ctx->in_cellof, cell_of, sizeof(int32_t) * n));
+  return run_host_table(ctx, MODE_CLL, *grid, n, d_x, nullptr, ctx->in_items.as<int32_t>(),
+                        ctx->in_start.as<int32_t>(), ctx->in_cellof.as<int32_t>(), precision, h,
+                        total);
+}
+
+int sphx_all_list(sphx_context* ctx, int32_t dim, int64_t n, const double* const x[3], double h,
+                  int32_t precision, int64_t* total) {
+  TRY(check_ctx(ctx));
+  if (!total) return fail(SPHX_ERR_INVALID_ARGUMENT, "null argument");
+  TRY(check_prec_dim(precision, dim));
+  if (n == 0) return fail(SPHX_ERR_INVALID_ARGUMENT, "all_list needs at least one particle");
+  sphx_grid_desc g;
+  std::memset(&g, 0, sizeof(g));
+  g.dim = dim;
+  for (int k = 0; k < 3; ++k) g.counts[k] = 1;
+  const double* d_x[3] = {nullptr, nullptr, nullptr};
+  for (int k = 0; k < dim; ++k) {
+    TRY(upload(ctx, ctx->in_x[k], x[k], sizeof(double) * n));
+    d_x[k] = ctx->in_x[k].as<double>();
+  }
+  return run_host_table(ctx, MODE_ALL, g, n, d_x, nullptr, nullptr, nullptr, nullptr, precision,
+                        h, total);
+}
+
+int sphx_table_copy(sphx_context* ctx, int64_t* offsets, int32_t* items) {
+  TRY(check_ctx(ctx));
+  if (ctx->t_n < 0) return fail(SPHX_ERR_INVALID_ARGUMENT, "no table computed on this context");
+  if (offsets)
+    CK(cudaMemcpyAsync(offsets, ctx->t_offsets.p, sizeof(int64_t) * (ctx->t_n + 1),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+  if (items && ctx->t_total)
+    CK(cudaMemcpyAsync(items, ctx->t_items.p, sizeof(int32_t) * ctx->t_total,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return SPHX_OK;
+}
+
+static int binning_host(sphx_context* ctx, int bmode, const sphx_grid_desc* grid, int64_t n,
+                        const double* const x[3], const int32_t* const cell_in[3],
+                        double* const rel[3], int32_t* const cell[3], int32_t* cell_of,
+                        int32_t* cell_start, int32_t* items) {
+  TRY(check_ctx(ctx));
+  if (!grid) return fail(SPHX_ERR_INVALID_ARGUMENT, "null grid");
+  TRY(check_prec_dim(SPHX_FP64, grid->dim));
+  if (n > INT32_MAX - 1024) return fail(SPHX_ERR_INVALID_ARGUMENT, "too many particles");
+  const int dim = grid->dim;
+  const int64_t C = cell_total(*grid);
+  const double* d_x[3] = {nullptr, nullptr, nullptr};
+  const int32_t* d_cin[3] = {nullptr, nullptr, nullptr};
+  double* d_rel[3] = {nullptr, nullptr, nullptr};
+  int32_t* d_cell[3] = {nullptr, nullptr, nullptr};
+  for (int k = 0; k < dim; ++k) {
+    if (bmode == 2) {
+      TRY(upload(ctx, ctx->in_cell[k], cell_in[k], sizeof(int32_t) * n));
+      d_cin[k] = ctx->in_cell[k].as<int32_t>();
+    } else {
+      TRY(upload(ctx, ctx->in_x[k], x[k], sizeof(double) * n));
+      d_x[k] = ctx->in_x[k].as<double>();
+    }
+    if (bmode == 1) {
+      TRY(ctx->b_rel[k].ensure(sizeof(double) * std::max<int64_t>(n, 1)));
+      TRY(ctx->b_cell[k].ensure(sizeof(int32_t) * std::max<int64_t>(n, 1)));
+      d_rel[k] = ctx->b_rel[k].as<double>();
+      d_cell[k] = ctx->b_cell[k].as<int32_t>();
+    }
+  }
+  TRY(ctx->b_out_cellof.ensure(sizeof(int32_t) * std::max<int64_t>(n, 1)));
+  TRY(ctx->b_out_start.ensure(sizeof(int32_t) * (C + 1)));
+  TRY(ctx->b_out_items.ensure(sizeof(int32_t) * std::max<int64_t>(n, 1)));
+  TRY(ctx->b_bad.ensure(sizeof(unsigned long long)));
+  CK(cudaMemsetAsync(ctx->b_bad.p, 0xFF, sizeof(unsigned long long), ctx->stream));
+  TRY(run_binning(ctx, bmode, *grid, n, d_x, d_cin, d_rel, d_cell, ctx->b_out_cellof.as<int32_t>(),
+                  ctx->b_out_start.as<int32_t>(), ctx->b_out_items.as<int32_t>(),
+                  ctx->b_bad.as<unsigned long long>()));
+  unsigned long long bad = ~0ull;
+  CK(cudaMemcpyAsync(&bad, ctx->b_bad.p, sizeof(bad), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (bad != ~0ull)
+    return fail(SPHX_ERR_OUT_OF_RANGE, "particle " + std::to_string(bad) + " lies outside the grid");
+  auto d2h = [&](void* dst, const void* src, size_t bytes) -> int {
+    if (dst && bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    return SPHX_OK;
+  };
+  TRY(d2h(cell_of, ctx->b_out_cellof.p, sizeof(int32_t) * n));
+  TRY(d2h(cell_start, ctx->b_out_start.p, sizeof(int32_t) * (C + 1)));
+  TRY(d2h(items, ctx->b_out_items.p, sizeof(int32_t) * n));
+  if (bmode == 1) {
+    for (int k = 0; k < dim; ++k) {
+      TRY(d2h(rel[k], d_rel[k], sizeof(double) * n));
+      TRY(d2h(cell[k], d_cell[k], sizeof(int32_t) * n));
+    }
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return SPHX_OK;
+}
+
+int sphx_rebin(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n, const double* const x[3],
+               int32_t* cell_of, int32_t* cell_start, int32_t* items) {
+  return binning_host(ctx, 0, grid, n, x, nullptr, nullptr, nullptr, cell_of, cell_start, items);
+}
+
+int sphx_build_rel_coords(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                          const double* const x[3], double* const rel[3], int32_t* const cell[3],
+                          int32_t* cell_of, int32_t* cell_start, int32_t* items) {
+  return binning_host(ctx, 1, grid, n, x, nullptr, rel, cell, cell_of, cell_start, items);
+}
+
+int sphx_rebuild_members(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                         const int32_t* const cell[3], int32_t* cell_of, int32_t* cell_start,
+                         int32_t* items) {
+  return binning_host(ctx, 2, grid, n, nullptr, cell, nullptr, nullptr, cell_of, cell_start,
+                      items);
+}
+
+// ---------------- device-resident API ----------------
+
+int sphx_rcll_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                     const double* const d_rel[3], const int32_t* const d_cell[3],
+                     const int32_t* d_items, const int32_t* d_cell_start, int32_t precision,
+                     int64_t* d_offsets, int32_t* d_items_out, int64_t capacity) {
+  TRY(check_ctx(ctx));
+  if (!grid) return fail(SPHX_ERR_INVALID_ARGUMENT, "null grid");
+  TRY(check_prec_dim(precision, grid->dim));
+  return run_nnps(ctx, MODE_RCLL, *grid, n, d_rel, d_cell, d_items, d_cell_start, nullptr,
+                  precision, 0.0, d_offsets, d_items_out, capacity, true);
+}
+
+int sphx_cell_link_list_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                               const double* const d_x[3], double h, const int32_t* d_items,
+                               const int32_t* d_cell_start, const int32_t* d_cell_of,
+                               int32_t precision, int64_t* d_offsets, int32_t* d_items_out,
+                               int64_t capacity) {
+  TRY(check_ctx(ctx));
+  if (!grid) return fail(SPHX_ERR_INVALID_ARGUMENT, "null grid");
+  TRY(check_prec_dim(precision, grid->dim));
+  return run_nnps(ctx, MODE_CLL, *grid, n, d_x, nullptr, d_items, d_cell_start, d_cell_of,
+                  precision, h, d_offsets, d_items_out, capacity, true);
+}
+
+int sphx_build_rel_coords_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                                 const double* const d_x[3], double* const d_rel[3],
+                                 int32_t* const d_cell[3], int32_t* d_cell_of,
+                                 int32_t* d_cell_start, int32_t* d_items) {
+  TRY(check_ctx(ctx));
+  if (!grid) return fail(SPHX_ERR_INVALID_ARGUMENT, "null grid");
+  TRY(check_prec_dim(SPHX_FP64, grid->dim));
+  TRY(ctx->b_bad.ensure(sizeof(unsigned long long)));
+  return run_binning(ctx, 1, *grid, n, d_x, nullptr, d_rel, d_cell, d_cell_of, d_cell_start,
+                     d_items, ctx->b_bad.as<unsigned long long>());
+}
+
+int sphx_rebin_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                      const double* const d_x[3], int32_t* d_cell_of, int32_t* d_cell_start,
+                      int32_t* d_items, int64_t* d_bad) {
+  TRY(check_ctx(ctx));
+  if (!grid || !d_bad) return fail(SPHX_ERR_INVALID_ARGUMENT, "null argument");
+  TRY(check_prec_dim(SPHX_FP64, grid->dim));
+  CK(cudaMemsetAsync(d_bad, 0xFF, sizeof(int64_t), ctx->stream));
+  return run_binning(ctx, 0, *grid, n, d_x, nullptr, nullptr, nullptr, d_cell_of, d_cell_start,
+                     d_items, reinterpret_cast<unsigned long long*>(d_bad));
+}
+
+}  // extern "C"

@@ -1,0 +1,131 @@
+// Shared device-side definitions for the sm_100a NNPS kernels.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sphx_dev {
+
+enum { FP64 = 0, FP32 = 1, FP16 = 2 };
+enum { MODE_RCLL = 0, MODE_CLL = 1, MODE_ALL = 2 };
+
+// Precision constants of one NNPS call, computed on the host so that they are
+// exactly the values the reference forms (nnps.cpp:287-295, :177-197):
+//   hh[k]  = round_to(prec, 0.5*hc[k])          (RCLL half cell edge)
+//   cc[k]  = round_to(prec, hc[k])              (RCLL centre difference, dc=+1;
+//                                                dc=-1 is its negation, dc=0 is 0)
+//   sh[k]  = round_to(prec, span[k])            (CLL periodic shift magnitude)
+//   thr    = smallest acc with finish(acc) >= round_to(prec, cutoff): the
+//            reference's sqrt-then-compare is replaced by the exact, monotone
+//            test acc < thr (SURVEY.md 8(c) "threshold trick").
+struct PrecConsts {
+  uint16_t h_hh[3], h_cc[3], h_sh[3], h_thr;
+  float f_hh[3], f_cc[3], f_sh[3], f_thr;
+  double d_hh[3], d_cc[3], d_sh[3], d_thr;
+};
+
+struct GridConsts {
+  int dim;
+  int counts[3];
+  int wrap[3];  // periodic(k) && count(k) > 2  (nnps.cpp:223, :364)
+};
+
+// Arguments of the fused sweep kernel.
+struct SweepArgs {
+  int n;
+  GridConsts g;
+  PrecConsts c;
+  const int32_t* cell_start;  // CellGrid::cell_start()  [C+1]
+  const int32_t* pid_s;       // CellGrid::items()       [n]  (CSR order -> particle id)
+  const void* pos_s;          // packed coords in CSR order
+  const void* pos_own;        // packed coords in particle order
+  const int32_t* cellk[3];    // RCLL: RelCoords::cell[k] (particle order)
+  const int32_t* cell_of;     // CLL:  CellGrid::cell_of  (particle order)
+  int64_t* offsets;           // [n+1]
+  int32_t* items;             // [capacity]
+  int64_t capacity;
+  unsigned long long* tiles;  // decoupled look-back state, one word per block
+  int* block_counter;         // dynamic block index
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ int warp_inclusive_scan(int v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  return v;
+}
+
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Decoupled look-back (single-pass prefix over blocks in dynamic launch order).
+// Called by all 32 lanes of one warp; returns the exclusive prefix of block `bid`.
+// Tile word: [63:62] flag (1 = aggregate, 2 = inclusive prefix), [61:0] value.
+__device__ __forceinline__ long long lookback_exclusive(unsigned long long* tiles, int bid,
+                                                        long long block_total) {
+  const unsigned long long AGG = 1ull << 62, PRE = 2ull << 62, VAL = (1ull << 62) - 1;
+  const int lane = threadIdx.x & 31;
+  if (bid == 0) {
+    if (lane == 0) st_release_u64(&tiles[0], PRE | (unsigned long long)block_total);
+    return 0;
+  }
+  if (lane == 0) st_release_u64(&tiles[bid], AGG | (unsigned long long)block_total);
+  long long excl = 0;
+  int p = bid - 1;
+  while (true) {
+    const int idx = p - lane;
+    const unsigned long long st = idx >= 0 ? ld_acquire_u64(&tiles[idx]) : PRE;
+    const unsigned flag = (unsigned)(st >> 62);
+    const unsigned pre_mask = __ballot_sync(0xffffffffu, flag == 2u);
+    const unsigned zero_mask = __ballot_sync(0xffffffffu, flag == 0u);
+    const int first = pre_mask ? __ffs(pre_mask) - 1 : 32;
+    const unsigned need = first >= 31 ? 0xffffffffu : ((2u << first) - 1u);
+    if (zero_mask & need) continue;  // a predecessor has not published yet
+    const long long v = lane <= first ? (long long)(st & VAL) : 0ll;
+    excl += warp_sum_ll(v);
+    if (first < 32) break;
+    p -= 32;
+  }
+  if (lane == 0) st_release_u64(&tiles[bid], PRE | (unsigned long long)(excl + block_total));
+  return excl;
+}
+
+// Binning (binning.cu)
+struct BinConsts {
+  int dim;
+  int counts[3];
+  double hc[3], origin[3], lo[3], hi[3];
+  double hd;
+};
+
+struct LocateArgs {
+  int n;
+  BinConsts g;
+  const double* x[3];
+  const int32_t* cell_in[3];  // BIN_MEMBERS
+  double* rel_out[3];         // BIN_REL
+  int32_t* cell_out[3];       // BIN_REL
+  int32_t* cell_of;
+  int32_t* counts;  // [C], zeroed
+  int32_t* slot;    // [n]
+  unsigned long long* bad;  // BIN_REBIN: min out-of-grid index
+};
+
+}  // namespace sphx_dev
