@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""NNPS benchmark (driver contract): FP16 RCLL neighbour search on the
+BASELINE config C2 (2-D jittered lattice 1000x1000 = 1M particles).
+
+A *step* is one drop-in ``rcll(rel, grid, fp16)`` call on device-resident inputs
+(RelCoords + CellGrid CSR in HBM) producing the contract-exact CSR neighbour table
+in HBM: encode kernel + fused sweep kernel. ``e2e`` is the same call through the
+C ABI with pinned host buffers (H2D of the inputs and D2H of the whole table
+inside the timed region). ``--impl reference`` times the reference's own CPU
+implementation (oracle/_ref, all host threads) on the same workload.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "NNPS particles/s at 1M particles (FP16 RCLL); achieved HBM GB/s vs peak"
+A100_SORTED_PPS = 1.0e6 / 2.60e-3  # paper Table 6, FP16 RCLL 1M sorted, A100
+
+WORKLOADS = {
+    "C1": dict(dim=2, ds=0.01, jitter=0.0, seed=1,
+               desc="C1 2-D lattice 100x100 (10K), FP16 RCLL"),
+    "C2": dict(dim=2, ds=0.001, jitter=0.3, seed=1,
+               desc="C2 2-D jittered lattice 1000x1000 (1M particles), FP16 RCLL"),
+    "C3": dict(dim=3, ds=0.01, jitter=0.3, seed=1,
+               desc="C3 3-D jittered lattice 100^3 (1M particles), FP16 RCLL, 27-cell sweep"),
+}
+PREC = {"fp64": 0, "fp32": 1, "fp16": 2}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--precision", default="fp16", choices=sorted(PREC))
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def golden(config, precision):
+    with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as f:
+        return json.load(f)["configs"][config]["tables"][f"rcll_{precision}"]
+
+
+def ncu_traffic(config, precision):
+    """Per-launch DRAM bytes of the sweep kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_sweep_summary.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    e = d.get(f"{config}_{precision}")
+    return None if e is None else e.get("dram_bytes")
+
+
+# ---------------------------------------------------------------------------------------
+# clocks during the timed region (NVML)
+# ---------------------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, device_index: int):
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def sample(self):
+        if self.nv is None:
+            return
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            self.reasons |= int(r) & ~0x1
+        except Exception:
+            pass
+
+    def _run(self):
+        while not self._stop.is_set():
+            self.sample()
+            time.sleep(0.005)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self.t.join()
+
+    def summary(self):
+        reasons = [name for bit, name in self.REASONS.items() if self.reasons & bit]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------------------
+# distributed plumbing (one process per GPU; N>1 via torchrun)
+# ---------------------------------------------------------------------------------------
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------------------
+# reference arm: the reference's own CPU implementation
+# ---------------------------------------------------------------------------------------
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle as O
+    w = WORKLOADS[args.config]
+    prec = PREC[args.precision]
+    cores = os.cpu_count() or 1
+    if os.path.exists(O.REF_SO):
+        kind = "reference"
+        lib = O.ref_lib()
+        lib.ref_set_threads(cores)
+        r = O.RefSystem.lattice(w["dim"], w["ds"], w["jitter"], w["seed"]).make_grid()
+        n = r.n
+        step = lambda: r.lib.ref_time_nnps(0, r.ps, r.rel, r.grid, prec, 1)  # noqa: E731
+        threads = lib.ref_max_threads()
+    else:  # the C restatement (single thread)
+        kind = "port"
+        orc = O.Oracle()
+        x = orc.lattice(w["dim"], w["ds"], w["jitter"], w["seed"])
+        g = orc.grid(w["dim"], 2.4 * w["ds"])
+        rel, cell, _, start, items = orc.build_rel(g, x)
+        n = len(x[0])
+
+        def step():
+            t0 = time.perf_counter()
+            orc.rcll(g, rel, cell, items, start, prec)
+            return time.perf_counter() - t0
+        threads = 1
+    for _ in range(args.warmup):
+        step()
+    ts = [step() for _ in range(args.steps)]
+    # ref_time_nnps(…, repeats=1) = one discarded warm-up + one timed call per step
+    t = statistics.mean(ts)
+    v = n / t
+    line = {"metric": METRIC, "value": v, "unit": "particles/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": w["desc"], "n_particles": n, "precision": args.precision,
+                       "backend": "rcll"},
+            "cpu_baseline": {"value": v, "unit": "particles/s", "cores": threads, "kind": kind,
+                             "sample": f"full {args.config} per step, rcll() only (grid and "
+                                       "RelCoords built outside the timer, experiments.cpp:"
+                                       "268-300)"},
+            "e2e": {"value": v, "unit": "particles/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(config, precision):
+    """Reference CPU path on this host's cores (bounded sample: one full C2 call,
+    median of 3 after a discarded warm-up)."""
+    import oracle as O
+    w = WORKLOADS[config]
+    prec = PREC[precision]
+    cores = os.cpu_count() or 1
+    try:
+        if os.path.exists(O.REF_SO):
+            lib = O.ref_lib()
+            lib.ref_set_threads(cores)
+            r = O.RefSystem.lattice(w["dim"], w["ds"], w["jitter"], w["seed"]).make_grid()
+            t = r.time_nnps("rcll", prec, repeats=3)
+            return {"value": r.n / t, "unit": "particles/s", "cores": lib.ref_max_threads(),
+                    "kind": "reference",
+                    "sample": f"full {config} ({r.n} particles) rcll() median of 3 after a "
+                              "warm-up, grid+RelCoords outside the timer"}
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "unit": "particles/s", "cores": cores, "kind": "reference",
+                "sample": f"failed: {e}"}
+    return None
+
+
+# ---------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+
+    import paper_2401_08586_b200 as P
+
+    world, rank, local = dist_env()
+    if world > 1:
+        from paper_2401_08586_b200 import multigpu
+        return multigpu.bench(args, WORKLOADS, METRIC)
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    # a dedicated (non-default) stream: the library and the L2 flush share it
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    w = WORKLOADS[args.config]
+    prec = PREC[args.precision]
+    dim, ds = w["dim"], w["ds"]
+    h = 1.2 * ds
+
+    # inputs: reference generator -> HBM; device binning + RCLL encoding (Eq. 5-6)
+    x = P.build_lattice(dim, ds, w["jitter"], w["seed"])
+    n = len(x[0])
+    grid = P.grid_init(dim, (0, 0, 0), (1, 1, 1), 2.0 * h)
+    C = grid.cell_total
+    ctx = P.Context(local)
+    ctx.set_stream(stream.cuda_stream)
+    xd = [torch.from_numpy(a).to(dev) for a in x]
+    rel = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(dim)]
+    cell = [torch.empty(n, dtype=torch.int32, device=dev) for _ in range(dim)]
+    cell_of = torch.empty(n, dtype=torch.int32, device=dev)
+    start = torch.empty(C + 1, dtype=torch.int32, device=dev)
+    items = torch.empty(n, dtype=torch.int32, device=dev)
+    ctx.build_rel_coords_device(grid, xd, rel, cell, cell_of, start, items)
+    offsets = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    cap = n * (24 if dim == 2 else 80)
+    out = torch.empty(cap, dtype=torch.int32, device=dev)
+
+    def step():
+        ctx.rcll_device(grid, rel, cell, items, start, prec, offsets, out)
+
+    step()
+    torch.cuda.synchronize()
+    total = int(offsets[-1])
+    if total > cap:
+        out = torch.empty(total, dtype=torch.int32, device=dev)
+        step()
+        torch.cuda.synchronize()
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > L2 (126 MB)
+    ctx.enable_timing(True)
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+
+    launches0 = ctx.launches
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    sweep_ms, encode_ms = [], []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        t_wall0 = time.perf_counter()
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+            e_ms, s_ms = ctx.last_timing()  # CUDA events around the two kernels
+            encode_ms.append(e_ms)
+            sweep_ms.append(s_ms)
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall0
+        gpu_launches = ctx.launches - launches0
+        step_ms = [a.elapsed_time(b) for a, b in ev]
+
+        # ---- e2e through the C ABI with pinned host buffers --------------------------
+        ctx.enable_timing(False)
+        ctx.set_stream(None)
+        pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+        h_rel = [pin(t) for t in rel]
+        h_cell = [pin(t) for t in cell]
+        h_items, h_start = pin(items), pin(start)
+        h_off = torch.empty(n + 1, dtype=torch.int64).pin_memory()
+        h_out = torch.empty(total, dtype=torch.int32).pin_memory()
+        rp = [t.data_ptr() for t in h_rel]
+        cp = [t.data_ptr() for t in h_cell]
+        for _ in range(2):
+            ctx.rcll_ptr(grid, n, rp, cp, h_items.data_ptr(), h_start.data_ptr(), prec)
+            ctx.table_copy_ptr(h_off.data_ptr(), h_out.data_ptr())
+        e2e_t = []
+        for _ in range(args.e2e_steps):
+            t0 = time.perf_counter()
+            tot = ctx.rcll_ptr(grid, n, rp, cp, h_items.data_ptr(), h_start.data_ptr(), prec)
+            ctx.table_copy_ptr(h_off.data_ptr(), h_out.data_ptr())
+            e2e_t.append(time.perf_counter() - t0)
+        assert tot == total
+
+    # ---- parity of the timed output with the reference's golden hash --------------------
+    gold = golden(args.config, args.precision)
+    dev_hash = P.capi.table_hash(offsets.cpu().numpy(), out[:total].cpu().numpy())
+    e2e_hash = P.capi.table_hash(h_off.numpy(), h_out.numpy())
+    parity = (total == gold["total"] and f"{dev_hash:016x}" == gold["hash"]
+              and e2e_hash == dev_hash)
+
+    t_step = statistics.mean(step_ms) * 1e-3
+    t_sweep = statistics.mean(sweep_ms) * 1e-3
+    t_e2e = statistics.mean(e2e_t)
+    s_pos = {0: 8, 1: 4, 2: 2}[prec] * dim
+    b_sweep = n * s_pos + 4 * n + 4 * (C + 1) + 8 * (n + 1) + 4 * total
+    peak, peak_kind = measured_peaks()
+    achieved = b_sweep / t_sweep / 1e9
+    h2d = sum(t.numel() * t.element_size() for t in h_rel + h_cell + [h_items, h_start])
+    d2h = (n + 1) * 8 + total * 4 + 8
+    line = {
+        "metric": METRIC, "value": n / t_step, "unit": "particles/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+        "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": (n / t_step) / A100_SORTED_PPS,
+        "vs_baseline_basis": "BASELINE.md: paper Table 6 FP16 RCLL 1M sorted on A100, 2.60 ms",
+        "dtype": "f16" if prec == 2 else ("f32" if prec == 1 else "f64"),
+        "data": "synthetic (reference build_lattice generator, seed 1)",
+        "config": {"workload": w["desc"], "n_particles": n, "cells": C, "pairs": total,
+                   "precision": args.precision, "backend": "rcll",
+                   "input": "device-resident RelCoords (fp64) + CellGrid CSR",
+                   "l2": "flushed between timed steps (256 MiB write, outside the events)"},
+        "parity": {"bit_exact_vs_reference_hash": parity, "hash": f"{dev_hash:016x}",
+                   "golden": gold["hash"]},
+        "breakdown_ms": {"encode": statistics.mean(encode_ms), "sweep": t_sweep * 1e3,
+                         "step": t_step * 1e3, "wall_per_step": t_wall / args.steps * 1e3},
+        "roofline": {"bound": "hbm", "kernel": "k_sweep (fused sweep+sort+scan+fill)",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": ncu_traffic(args.config, args.precision),
+                     "algorithmic_bytes": b_sweep,
+                     "bytes_formula": "N*S_pos + 4N + 4(C+1) + 8(N+1) + 4P"},
+        "e2e": {"value": n / t_e2e, "unit": "particles/s", "ms_per_step": t_e2e * 1e3,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "api": "sphx_rcll + sphx_table_copy (C ABI), pinned host buffers"},
+        "gpu_launches": gpu_launches,
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.config, args.precision)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -165,6 +165,22 @@ int sphx_rebin_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
                       const double* const d_x[3], int32_t* d_cell_of, int32_t* d_cell_start,
                       int32_t* d_items, int64_t* d_bad);
 
+/* ---------------- synthetic inputs ---------------- */
+
+/* build_lattice(Domain::box(dim, lo, hi), ds, jitter, seed) (particle_system.hpp:66,
+ * particle_system.cpp:31-62): cell-centred lattice, x fastest, per-axis jitter
+ * jitter*ds*(2u-1) from mt19937_64. Call with x0 == NULL to get *n only. */
+int sphx_build_lattice(int32_t dim, const double lo[3], const double hi[3], double ds,
+                       double jitter, uint64_t seed, int64_t* n, double* x0, double* x1,
+                       double* x2);
+/* build_random_uniform (particle_system.hpp:70, particle_system.cpp:64-77). */
+int sphx_build_random_uniform(int32_t dim, const double lo[3], const double hi[3], int64_t n,
+                              uint64_t seed, double* ds, double* x0, double* x1, double* x2);
+
+/* FNV-1a 64 digest of a CSR table (offsets as u64, then items as u32): the
+ * golden-vector hash of tests/golden/golden.json. Host memory, pure host code. */
+uint64_t sphx_table_hash(const int64_t* offsets, int64_t n, const int32_t* items, int64_t total);
+
 /* Per-kernel timing of the last sphx_*_device NNPS call when timing is enabled
  * (CUDA events on the launching stream): encode and sweep in milliseconds. */
 int sphx_enable_timing(sphx_context* ctx, int on);

@@ -80,7 +80,12 @@ def lib():
         "sphx_build_rel_coords_device": (C.c_int, [vp, G, i64, p3, p3, p3, vp, vp, vp]),
         "sphx_rebin_device": (C.c_int, [vp, G, i64, p3, vp, vp, vp, vp]),
         "sphx_enable_timing": (C.c_int, [vp, C.c_int]),
+        "sphx_build_lattice": (C.c_int, [i32, C.POINTER(dbl), C.POINTER(dbl), dbl, dbl,
+                                         C.c_uint64, C.POINTER(i64), vp, vp, vp]),
+        "sphx_build_random_uniform": (C.c_int, [i32, C.POINTER(dbl), C.POINTER(dbl), i64,
+                                                C.c_uint64, C.POINTER(dbl), vp, vp, vp]),
         "sphx_last_timing": (C.c_int, [vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+        "sphx_table_hash": (C.c_uint64, [vp, i64, vp, i64]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -95,7 +100,15 @@ EXPORTED = ("sphx_last_error", "sphx_grid_init", "sphx_create", "sphx_destroy",
             "sphx_all_list", "sphx_table_copy", "sphx_rebin", "sphx_build_rel_coords",
             "sphx_rebuild_members", "sphx_rcll_device", "sphx_cell_link_list_device",
             "sphx_build_rel_coords_device", "sphx_rebin_device", "sphx_enable_timing",
-            "sphx_last_timing")
+            "sphx_last_timing", "sphx_build_lattice", "sphx_build_random_uniform",
+            "sphx_table_hash")
+
+
+def table_hash(offsets: np.ndarray, items: np.ndarray) -> int:
+    """FNV-1a 64 table digest (the golden-vector hash)."""
+    o = np.ascontiguousarray(offsets, np.int64)
+    it = np.ascontiguousarray(items, np.int32)
+    return int(lib().sphx_table_hash(o.ctypes.data, len(o) - 1, it.ctypes.data, len(it)))
 
 
 def check(rc: int) -> None:
@@ -123,6 +136,26 @@ def grid_init(dim: int, lo, hi, radius: float, periodic=(0, 0, 0)) -> GridDesc:
     p = (C.c_int32 * 3)(*[int(bool(x)) for x in list(periodic) + [0] * (3 - len(periodic))])
     check(lib().sphx_grid_init(C.byref(g), dim, _d3(lo), _d3(hi), float(radius), p))
     return g
+
+
+def build_lattice(dim: int, ds: float, jitter: float, seed: int, lo=(0, 0, 0), hi=(1, 1, 1)):
+    """ParticleSystem positions of build_lattice (particle_system.cpp:31-62)."""
+    n = C.c_int64()
+    check(lib().sphx_build_lattice(dim, _d3(lo), _d3(hi), ds, jitter, seed, C.byref(n),
+                                   None, None, None))
+    xs = [np.empty(n.value, np.float64) for _ in range(dim)]
+    check(lib().sphx_build_lattice(dim, _d3(lo), _d3(hi), ds, jitter, seed, C.byref(n),
+                                   *[x.ctypes.data for x in xs], *([None] * (3 - dim))))
+    return xs
+
+
+def build_random_uniform(dim: int, n: int, seed: int, lo=(0, 0, 0), hi=(1, 1, 1)):
+    """Positions and ds of build_random_uniform (particle_system.cpp:64-77)."""
+    xs = [np.empty(n, np.float64) for _ in range(dim)]
+    ds = C.c_double()
+    check(lib().sphx_build_random_uniform(dim, _d3(lo), _d3(hi), n, seed, C.byref(ds),
+                                          *[x.ctypes.data for x in xs], *([None] * (3 - dim))))
+    return xs, ds.value
 
 
 def _ptr3(arrs):
@@ -247,6 +280,19 @@ class Context:
                                          cell_of.ctypes.data, start.ctypes.data,
                                          items.ctypes.data))
         return cell_of[:n], start, items[:n]
+
+    # ---- raw host pointers (e.g. pinned torch CPU tensors) ------------------------------
+    def rcll_ptr(self, grid: GridDesc, n: int, rel_ptrs, cell_ptrs, items_ptr: int,
+                 start_ptr: int, prec: int) -> int:
+        tot = C.c_int64()
+        r = (C.c_void_p * 3)(*(list(rel_ptrs) + [None] * (3 - len(rel_ptrs))))
+        c = (C.c_void_p * 3)(*(list(cell_ptrs) + [None] * (3 - len(cell_ptrs))))
+        check(lib().sphx_rcll(self.h, C.byref(grid), n, r, c, n, items_ptr, start_ptr, prec,
+                              C.byref(tot)))
+        return tot.value
+
+    def table_copy_ptr(self, offsets_ptr: int, items_ptr: int) -> None:
+        check(lib().sphx_table_copy(self.h, offsets_ptr, items_ptr))
 
     # ---- device-resident API (torch tensors as device memory) ---------------------------
     def rcll_device(self, grid, rel, cell, items, cell_start, prec, offsets, items_out):

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <random>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -16,12 +17,15 @@
 
 namespace sphx_dev {
 // sweep.cu
-void launch_encode(int dim, int prec, int n, const double* const x[3], const int32_t* items,
-                   void* own, void* pos_s, unsigned long long* tiles, int ntiles, int* counter,
-                   cudaStream_t st);
-void launch_sweep(int dim, int prec, int mode, const SweepArgs& a, cudaStream_t st);
+int launch_encode(int dim, int prec, int mode, int n, int64_t C, int nx, int wrapx,
+                  const double* const x[3], const int32_t* items, const int32_t* start,
+                  void* own, int2* tri, void* rec, cudaStream_t st);
+void launch_count(int dim, int prec, int mode, const SweepArgs& a, cudaStream_t st);
+void launch_fill(int dim, int prec, int mode, const SweepArgs& a, cudaStream_t st);
 size_t coord_bytes(int dim, int prec);
-int sweep_block_threads(int dim);
+size_t record_bytes(int dim, int prec);
+int sweep_block_rows(int dim);
+int mask_words(int dim);
 // binning.cu
 int64_t scan_tiles(int64_t C);
 void launch_locate(int mode, const LocateArgs& a, cudaStream_t st);
@@ -110,7 +114,7 @@ struct sphx_context {
   // inputs staged from host
   Buf in_x[3], in_cell[3], in_items, in_start, in_cellof;
   // encode / sweep scratch
-  Buf pos_own, pos_s, tiles, counter;
+  Buf pos_own, tri, rec, counts, block_sum, masks;
   // table of the last host-API call
   Buf t_offsets, t_items;
   int64_t t_n = -1, t_total = 0, t_capacity = 0;
@@ -250,97 +254,106 @@ int upload(sphx_context* ctx, Buf& b, const void* src, size_t bytes) {
   return SPHX_OK;
 }
 
-// Encode + sweep on device pointers. src = rel (RCLL) or positions (CLL/ALL).
-int run_nnps(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n64,
-             const double* const src[3], const int32_t* const cellk[3], const int32_t* items,
-             const int32_t* start, const int32_t* cell_of, int prec, double h, int64_t* d_off,
-             int32_t* d_items, int64_t capacity, bool encode) {
-  if (n64 > INT32_MAX - 1024) return fail(SPHX_ERR_INVALID_ARGUMENT, "too many particles for int32 ids");
+// Encode + count + block-sum scan on device pointers (src = rel for RCLL,
+// positions for CLL/ALL). Leaves the exact total in d_off[n] and the sweep
+// arguments in *out for the fill pass.
+int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n64,
+                const double* const src[3], const int32_t* const cellk[3], const int32_t* items,
+                const int32_t* start, const int32_t* cell_of, int prec, double h, int64_t* d_off,
+                SweepArgs* out) {
+  // record tags hold id << 2 in 32 bits
+  if (n64 >= (int64_t(1) << 30))
+    return fail(SPHX_ERR_INVALID_ARGUMENT, "too many particles for one context (limit 2^30)");
   const int n = (int)n64;
   cudaStream_t st = ctx->stream;
+  std::memset(out, 0, sizeof(*out));
+  out->n = n;
   if (n == 0) {
     CK(cudaMemsetAsync(d_off, 0, sizeof(int64_t), st));
     return SPHX_OK;
   }
-  const size_t cb = coord_bytes(g.dim, prec);
-  const int bt = sweep_block_threads(g.dim);
-  const int nblocks = (n + bt - 1) / bt;
-  TRY(ctx->pos_own.ensure(cb * n));
-  if (mode != MODE_ALL) TRY(ctx->pos_s.ensure(cb * n));
-  TRY(ctx->tiles.ensure(sizeof(unsigned long long) * nblocks));
-  TRY(ctx->counter.ensure(sizeof(int)));
+  const int64_t C = mode == MODE_ALL ? 0 : cell_total(g);
+  const int nb = (n + sweep_block_rows(g.dim) - 1) / sweep_block_rows(g.dim);
+  // chunks of 4 may read up to 3 entries past a run: pad the candidate arrays
+  TRY(ctx->pos_own.ensure(coord_bytes(g.dim, prec) * (n + 4)));
+  if (mode != MODE_ALL) {
+    TRY(ctx->tri.ensure(sizeof(int2) * std::max<int64_t>(C, 1)));
+    TRY(ctx->rec.ensure(record_bytes(g.dim, prec) * (3 * (size_t)n + 4)));
+    TRY(ctx->masks.ensure(sizeof(unsigned) * mask_words(g.dim) * (size_t)n));
+  }
+  TRY(ctx->counts.ensure(sizeof(int32_t) * n));
+  TRY(ctx->block_sum.ensure(sizeof(long long) * nb));
 
   if (ctx->timing) CK(cudaEventRecord(ctx->ev[0], st));
-  if (encode) {
-    launch_encode(g.dim, prec, n, src, mode == MODE_ALL ? nullptr : items, ctx->pos_own.p,
-                  ctx->pos_s.p, ctx->tiles.as<unsigned long long>(), nblocks,
-                  ctx->counter.as<int>(), st);
-    CKL();
-    ++ctx->launches;
-  } else {
-    CK(cudaMemsetAsync(ctx->tiles.p, 0, sizeof(unsigned long long) * nblocks, st));
-    CK(cudaMemsetAsync(ctx->counter.p, 0, sizeof(int), st));
-  }
+  const GridConsts gc = grid_consts(g);
+  ctx->launches += launch_encode(g.dim, prec, mode, n, C, gc.counts[0], gc.wrap[0], src, items,
+                                 start, ctx->pos_own.p, ctx->tri.as<int2>(), ctx->rec.p, st);
+  CKL();
   if (ctx->timing) CK(cudaEventRecord(ctx->ev[1], st));
 
-  SweepArgs a;
-  std::memset(&a, 0, sizeof(a));
-  a.n = n;
-  a.g = grid_consts(g);
+  SweepArgs& a = *out;
+  a.g = gc;
   a.c = make_consts(mode, prec, g, h);
-  a.cell_start = start;
-  a.pid_s = items;
+  a.tri = ctx->tri.as<int2>();
+  a.rec = ctx->rec.p;
   a.pos_own = ctx->pos_own.p;
-  a.pos_s = mode == MODE_ALL ? ctx->pos_own.p : ctx->pos_s.p;
   for (int k = 0; k < 3; ++k) a.cellk[k] = cellk ? cellk[k] : nullptr;
   a.cell_of = cell_of;
   a.offsets = d_off;
-  a.items = d_items;
-  a.capacity = capacity;
-  a.tiles = ctx->tiles.as<unsigned long long>();
-  a.block_counter = ctx->counter.as<int>();
-  launch_sweep(g.dim, prec, mode, a, st);
+  a.counts = ctx->counts.as<int32_t>();
+  a.masks = ctx->masks.as<unsigned>();
+  a.block_sum = ctx->block_sum.as<long long>();
+  launch_count(g.dim, prec, mode, a, st);
   CKL();
-  ++ctx->launches;
-  if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], st));
+  ctx->launches += 2;
   return SPHX_OK;
 }
 
-// Host-API driver: stage, run, read the total, grow + re-run when needed.
+int run_fill(sphx_context* ctx, int mode, int dim, int prec, SweepArgs& a, int32_t* d_items,
+             int64_t capacity) {
+  if (a.n == 0) return SPHX_OK;
+  a.items = d_items;
+  a.capacity = capacity;
+  launch_fill(dim, prec, mode, a, ctx->stream);
+  CKL();
+  ++ctx->launches;
+  if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], ctx->stream));
+  return SPHX_OK;
+}
+
+// Device API: all passes, no synchronisation (capacity overflow is detectable by
+// the caller through d_off[n]).
+int run_nnps(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n,
+             const double* const src[3], const int32_t* const cellk[3], const int32_t* items,
+             const int32_t* start, const int32_t* cell_of, int prec, double h, int64_t* d_off,
+             int32_t* d_items, int64_t capacity) {
+  SweepArgs a;
+  TRY(run_prepare(ctx, mode, g, n, src, cellk, items, start, cell_of, prec, h, d_off, &a));
+  return run_fill(ctx, mode, g.dim, prec, a, d_items, capacity);
+}
+
+// Host-API driver: count, read the exact total, size the table, fill.
 int run_host_table(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n,
                    const double* const d_src[3], const int32_t* const d_cellk[3],
                    const int32_t* d_items, const int32_t* d_start, const int32_t* d_cellof,
                    int prec, double h, int64_t* total) {
   TRY(ctx->t_offsets.ensure(sizeof(int64_t) * (n + 1)));
-  if (ctx->t_capacity < 1) {
-    const int64_t guess = n * (g.dim == 3 ? 80 : (g.dim == 2 ? 24 : 8));
-    ctx->t_capacity = std::max<int64_t>(guess, 1 << 16);
-  }
-  TRY(ctx->t_items.ensure(sizeof(int32_t) * ctx->t_capacity));
-  bool encode = true;
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    TRY(run_nnps(ctx, mode, g, n, d_src, d_cellk, d_items, d_start, d_cellof, prec, h,
-                 ctx->t_offsets.as<int64_t>(), ctx->t_items.as<int32_t>(), ctx->t_capacity,
-                 encode));
-    int64_t tot = 0;
-    CK(cudaMemcpyAsync(&tot, ctx->t_offsets.as<int64_t>() + n, sizeof(int64_t),
-                       cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    if (tot <= ctx->t_capacity) {
-      ctx->t_n = n;
-      ctx->t_total = tot;
-      *total = tot;
-      if (ctx->timing) {
-        cudaEventElapsedTime(&ctx->t_encode, ctx->ev[0], ctx->ev[1]);
-        cudaEventElapsedTime(&ctx->t_sweep, ctx->ev[1], ctx->ev[2]);
-      }
-      return SPHX_OK;
-    }
-    ctx->t_capacity = tot + tot / 8 + 1024;
+  SweepArgs a;
+  TRY(run_prepare(ctx, mode, g, n, d_src, d_cellk, d_items, d_start, d_cellof, prec, h,
+                  ctx->t_offsets.as<int64_t>(), &a));
+  int64_t tot = 0;
+  CK(cudaMemcpyAsync(&tot, ctx->t_offsets.as<int64_t>() + n, sizeof(int64_t),
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (tot > ctx->t_capacity) {
+    ctx->t_capacity = tot + tot / 16 + 1024;
     TRY(ctx->t_items.ensure(sizeof(int32_t) * ctx->t_capacity));
-    encode = false;
   }
-  return fail(SPHX_ERR_RUNTIME, "neighbour table did not fit after regrowth");
+  TRY(run_fill(ctx, mode, g.dim, prec, a, ctx->t_items.as<int32_t>(), ctx->t_capacity));
+  ctx->t_n = n;
+  ctx->t_total = tot;
+  *total = tot;
+  return SPHX_OK;
 }
 
 int check_ctx(sphx_context* ctx) {
@@ -473,7 +486,7 @@ void sphx_destroy(sphx_context* ctx) {
   cudaStreamSynchronize(ctx->stream);
   Buf* all[] = {&ctx->in_x[0], &ctx->in_x[1], &ctx->in_x[2], &ctx->in_cell[0], &ctx->in_cell[1],
                 &ctx->in_cell[2], &ctx->in_items, &ctx->in_start, &ctx->in_cellof, &ctx->pos_own,
-                &ctx->pos_s, &ctx->tiles, &ctx->counter, &ctx->t_offsets, &ctx->t_items,
+                &ctx->tri, &ctx->rec, &ctx->counts, &ctx->block_sum, &ctx->masks, &ctx->t_offsets, &ctx->t_items,
                 &ctx->b_counts, &ctx->b_slot, &ctx->b_bad, &ctx->b_tiles, &ctx->b_out_cellof,
                 &ctx->b_out_start, &ctx->b_out_items, &ctx->b_rel[0], &ctx->b_rel[1],
                 &ctx->b_rel[2], &ctx->b_cell[0], &ctx->b_cell[1], &ctx->b_cell[2]};
@@ -677,7 +690,7 @@ int sphx_rcll_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
   if (!grid) return fail(SPHX_ERR_INVALID_ARGUMENT, "null grid");
   TRY(check_prec_dim(precision, grid->dim));
   return run_nnps(ctx, MODE_RCLL, *grid, n, d_rel, d_cell, d_items, d_cell_start, nullptr,
-                  precision, 0.0, d_offsets, d_items_out, capacity, true);
+                  precision, 0.0, d_offsets, d_items_out, capacity);
 }
 
 int sphx_cell_link_list_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
@@ -689,7 +702,7 @@ int sphx_cell_link_list_device(sphx_context* ctx, const sphx_grid_desc* grid, in
   if (!grid) return fail(SPHX_ERR_INVALID_ARGUMENT, "null grid");
   TRY(check_prec_dim(precision, grid->dim));
   return run_nnps(ctx, MODE_CLL, *grid, n, d_x, nullptr, d_items, d_cell_start, d_cell_of,
-                  precision, h, d_offsets, d_items_out, capacity, true);
+                  precision, h, d_offsets, d_items_out, capacity);
 }
 
 int sphx_build_rel_coords_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
@@ -713,6 +726,71 @@ int sphx_rebin_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
   CK(cudaMemsetAsync(d_bad, 0xFF, sizeof(int64_t), ctx->stream));
   return run_binning(ctx, 0, *grid, n, d_x, nullptr, nullptr, nullptr, d_cell_of, d_cell_start,
                      d_items, reinterpret_cast<unsigned long long*>(d_bad));
+}
+
+// ---------------- synthetic inputs (particle_system.cpp:31-77) ----------------
+
+int sphx_build_lattice(int32_t dim, const double lo[3], const double hi[3], double ds,
+                       double jitter, uint64_t seed, int64_t* n_out, double* x0, double* x1,
+                       double* x2) {
+  if (!n_out) return fail(SPHX_ERR_INVALID_ARGUMENT, "null argument");
+  if (dim < 1 || dim > 3) return fail(SPHX_ERR_INVALID_ARGUMENT, "domain dimension must be 1, 2 or 3");
+  for (int k = 0; k < dim; ++k)
+    if (!(lo[k] < hi[k])) return fail(SPHX_ERR_INVALID_ARGUMENT, "domain bounds must satisfy lo < hi");
+  if (!(ds > 0.0)) return fail(SPHX_ERR_INVALID_ARGUMENT, "ds must be positive");
+  if (jitter < 0.0 || jitter >= 0.5) return fail(SPHX_ERR_INVALID_ARGUMENT, "jitter must be in [0, 0.5)");
+  int64_t counts[3] = {1, 1, 1}, n = 1;
+  for (int k = 0; k < dim; ++k) {
+    if (ds > hi[k] - lo[k]) return fail(SPHX_ERR_INVALID_ARGUMENT, "ds exceeds the smallest domain span");
+    counts[k] = static_cast<int64_t>(std::floor((hi[k] - lo[k]) / ds + 0.5));
+    n *= counts[k];
+  }
+  *n_out = n;
+  if (!x0) return SPHX_OK;  // size query
+  double* xs[3] = {x0, x1, x2};
+  std::mt19937_64 gen(seed);
+  auto u01 = [&] { return static_cast<double>(gen() >> 11) * 0x1.0p-53; };  // rng.hpp:15
+  int64_t idx = 0;
+  int64_t c[3];
+  for (c[2] = 0; c[2] < counts[2]; ++c[2])
+    for (c[1] = 0; c[1] < counts[1]; ++c[1])
+      for (c[0] = 0; c[0] < counts[0]; ++c[0]) {
+        for (int k = 0; k < dim; ++k) {
+          double v = lo[k] + (static_cast<double>(c[k]) + 0.5) * ds;
+          if (jitter > 0.0) v += jitter * ds * (2.0 * u01() - 1.0);
+          xs[k][idx] = v;
+        }
+        ++idx;
+      }
+  return SPHX_OK;
+}
+
+uint64_t sphx_table_hash(const int64_t* offsets, int64_t n, const int32_t* items, int64_t total) {
+  uint64_t x = 1469598103934665603ull;  // FNV-1a 64 over offsets (u64) then items (u32)
+  for (int64_t i = 0; i <= n; ++i) {
+    x ^= static_cast<uint64_t>(offsets[i]);
+    x *= 1099511628211ull;
+  }
+  for (int64_t q = 0; q < total; ++q) {
+    x ^= static_cast<uint32_t>(items[q]);
+    x *= 1099511628211ull;
+  }
+  return x;
+}
+
+int sphx_build_random_uniform(int32_t dim, const double lo[3], const double hi[3], int64_t n,
+                              uint64_t seed, double* ds_out, double* x0, double* x1, double* x2) {
+  if (dim < 1 || dim > 3) return fail(SPHX_ERR_INVALID_ARGUMENT, "domain dimension must be 1, 2 or 3");
+  if (n < 1) return fail(SPHX_ERR_INVALID_ARGUMENT, "n must be at least 1");
+  double vol = 1.0;
+  for (int k = 0; k < dim; ++k) vol *= hi[k] - lo[k];
+  if (ds_out) *ds_out = std::pow(vol / static_cast<double>(n), 1.0 / dim);
+  double* xs[3] = {x0, x1, x2};
+  std::mt19937_64 gen(seed);
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < dim; ++k)
+      xs[k][i] = lo[k] + (hi[k] - lo[k]) * (static_cast<double>(gen() >> 11) * 0x1.0p-53);
+  return SPHX_OK;
 }
 
 }  // extern "C"

@@ -36,27 +36,30 @@ struct SweepArgs {
   int n;
   GridConsts g;
   PrecConsts c;
-  const int32_t* cell_start;  // CellGrid::cell_start()  [C+1]
-  const int32_t* pid_s;       // CellGrid::items()       [n]  (CSR order -> particle id)
-  const void* pos_s;          // packed coords in CSR order
+  const int2* tri;            // [C] record run [x, y) of each cell's x-triple
+  const void* rec;            // candidate records (coords + id << 2 | x code), <= 3n
   const void* pos_own;        // packed coords in particle order
   const int32_t* cellk[3];    // RCLL: RelCoords::cell[k] (particle order)
   const int32_t* cell_of;     // CLL:  CellGrid::cell_of  (particle order)
   int64_t* offsets;           // [n+1]
   int32_t* items;             // [capacity]
   int64_t capacity;
-  unsigned long long* tiles;  // decoupled look-back state, one word per block
-  int* block_counter;         // dynamic block index
+  int32_t* counts;            // [n] row lengths (pass 1), bit 31: masks overflowed
+  unsigned* masks;            // [W][n] hit nibbles of every 4-record chunk (pass 1)
+  long long* block_sum;       // [blocks] row-length sums, scanned in place (pass 2)
 };
 
+// Look-back words carry flag and value in one 64-bit word, so relaxed gpu-scope
+// accesses suffice. (An acquire load would compile to CCTL.IVALL -- an L1
+// invalidation per spin iteration that evicts every warp's cached candidates.)
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
   unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 
 __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 __device__ __forceinline__ int warp_inclusive_scan(int v) {
@@ -89,6 +92,9 @@ __device__ __forceinline__ long long lookback_exclusive(unsigned long long* tile
   if (lane == 0) st_release_u64(&tiles[bid], AGG | (unsigned long long)block_total);
   long long excl = 0;
   int p = bid - 1;
+  unsigned backoff = 32;
+  // windows of 32 predecessors; a window that is not fully published is re-polled
+  // after a short sleep so that waiting warps do not steal issue slots
   while (true) {
     const int idx = p - lane;
     const unsigned long long st = idx >= 0 ? ld_acquire_u64(&tiles[idx]) : PRE;
@@ -97,7 +103,11 @@ __device__ __forceinline__ long long lookback_exclusive(unsigned long long* tile
     const unsigned zero_mask = __ballot_sync(0xffffffffu, flag == 0u);
     const int first = pre_mask ? __ffs(pre_mask) - 1 : 32;
     const unsigned need = first >= 31 ? 0xffffffffu : ((2u << first) - 1u);
-    if (zero_mask & need) continue;  // a predecessor has not published yet
+    if (zero_mask & need) {
+      __nanosleep(backoff);
+      backoff = backoff < 1024 ? backoff * 2 : 1024;
+      continue;
+    }
     const long long v = lane <= first ? (long long)(st & VAL) : 0ll;
     excl += warp_sum_ll(v);
     if (first < 32) break;

@@ -68,3 +68,18 @@ def test_no_cpu_fallback_without_gpu():
     from paper_2401_08586_b200 import capi
     with pytest.raises(capi.SphxCudaError):
         capi.Context(0)
+
+
+@pytest.mark.parametrize("dim,ds,jit,seed", [(2, 0.01, 0.3, 1), (3, 0.05, 0.2, 7), (1, 0.1, 0.0, 3)])
+def test_generators_match_reference(dim, ds, jit, seed):
+    import oracle as O
+    import paper_2401_08586_b200 as P
+    want = O.Oracle().lattice(dim, ds, jit, seed)
+    got = P.build_lattice(dim, ds, jit, seed)
+    for a, b in zip(got, want):
+        assert np.array_equal(a, b)
+    want, wds = O.Oracle().random(dim, 777, seed)
+    got, gds = P.build_random_uniform(dim, 777, seed)
+    assert gds == wds
+    for a, b in zip(got, want):
+        assert np.array_equal(a, b)
