@@ -18,13 +18,15 @@
 namespace sphx_dev {
 // sweep.cu
 int launch_encode(int dim, int prec, int mode, int n, int64_t C, int nx, int wrapx,
-                  const double* const x[3], const int32_t* items, const int32_t* start,
-                  void* own, int2* tri, void* rec, cudaStream_t st);
+                  const PrecConsts& pc, const double* const x[3], const int32_t* items,
+                  const int32_t* start, void* pos_csr, int32_t* cell_slot, const SweepArgs& a,
+                  cudaStream_t st);
 void launch_count(int dim, int prec, int mode, const SweepArgs& a, cudaStream_t st);
 void launch_fill(int dim, int prec, int mode, const SweepArgs& a, cudaStream_t st);
 size_t coord_bytes(int dim, int prec);
-size_t record_bytes(int dim, int prec);
-int sweep_block_rows(int dim);
+size_t quad_bytes(int prec);
+int64_t chunk_capacity(int mode, int64_t n, int64_t C);
+int fill_tile(int dim);
 int mask_words(int dim);
 // binning.cu
 int64_t scan_tiles(int64_t C);
@@ -114,7 +116,7 @@ struct sphx_context {
   // inputs staged from host
   Buf in_x[3], in_cell[3], in_items, in_start, in_cellof;
   // encode / sweep scratch
-  Buf pos_own, tri, rec, counts, block_sum, masks;
+  Buf pos_own, pos_csr, cell_slot, tri, qx[3], qdc, qtag, rank, selfpos, counts, block_sum, masks;
   // table of the last host-API call
   Buf t_offsets, t_items;
   int64_t t_n = -1, t_total = 0, t_capacity = 0;
@@ -261,9 +263,8 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
                 const double* const src[3], const int32_t* const cellk[3], const int32_t* items,
                 const int32_t* start, const int32_t* cell_of, int prec, double h, int64_t* d_off,
                 SweepArgs* out) {
-  // record tags hold id << 2 in 32 bits
-  if (n64 >= (int64_t(1) << 30))
-    return fail(SPHX_ERR_INVALID_ARGUMENT, "too many particles for one context (limit 2^30)");
+  if (n64 > INT32_MAX - 64)
+    return fail(SPHX_ERR_INVALID_ARGUMENT, "too many particles for one context (int32 ids)");
   const int n = (int)n64;
   cudaStream_t st = ctx->stream;
   std::memset(out, 0, sizeof(*out));
@@ -273,29 +274,33 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
     return SPHX_OK;
   }
   const int64_t C = mode == MODE_ALL ? 0 : cell_total(g);
-  const int nb = (n + sweep_block_rows(g.dim) - 1) / sweep_block_rows(g.dim);
-  // chunks of 4 may read up to 3 entries past a run: pad the candidate arrays
-  TRY(ctx->pos_own.ensure(coord_bytes(g.dim, prec) * (n + 4)));
+  const int64_t chunks = chunk_capacity(mode, n, C);
+  const int nb = (n + fill_tile(g.dim) - 1) / fill_tile(g.dim);
+  TRY(ctx->pos_own.ensure(coord_bytes(g.dim, prec) * (size_t)n));
+  for (int k = 0; k < g.dim; ++k) TRY(ctx->qx[k].ensure(quad_bytes(prec) * (size_t)chunks));
+  TRY(ctx->qtag.ensure(16 * (size_t)chunks));
+  if (mode == MODE_RCLL) TRY(ctx->qdc.ensure(quad_bytes(prec) * (size_t)chunks));
   if (mode != MODE_ALL) {
+    TRY(ctx->pos_csr.ensure(coord_bytes(g.dim, prec) * (size_t)n));
+    TRY(ctx->cell_slot.ensure(sizeof(int32_t) * (size_t)n));
     TRY(ctx->tri.ensure(sizeof(int2) * std::max<int64_t>(C, 1)));
-    TRY(ctx->rec.ensure(record_bytes(g.dim, prec) * (3 * (size_t)n + 4)));
-    TRY(ctx->masks.ensure(sizeof(unsigned) * mask_words(g.dim) * (size_t)n));
+    TRY(ctx->rank.ensure(sizeof(int32_t) * (size_t)n));
+    TRY(ctx->selfpos.ensure(sizeof(int32_t) * (size_t)n));
   }
+  TRY(ctx->masks.ensure(sizeof(unsigned) * mask_words(g.dim) * (size_t)n));
   TRY(ctx->counts.ensure(sizeof(int32_t) * n));
   TRY(ctx->block_sum.ensure(sizeof(long long) * nb));
 
-  if (ctx->timing) CK(cudaEventRecord(ctx->ev[0], st));
-  const GridConsts gc = grid_consts(g);
-  ctx->launches += launch_encode(g.dim, prec, mode, n, C, gc.counts[0], gc.wrap[0], src, items,
-                                 start, ctx->pos_own.p, ctx->tri.as<int2>(), ctx->rec.p, st);
-  CKL();
-  if (ctx->timing) CK(cudaEventRecord(ctx->ev[1], st));
-
   SweepArgs& a = *out;
-  a.g = gc;
+  a.g = grid_consts(g);
   a.c = make_consts(mode, prec, g, h);
   a.tri = ctx->tri.as<int2>();
-  a.rec = ctx->rec.p;
+  for (int k = 0; k < 3; ++k) a.qx[k] = ctx->qx[k].p;
+  a.qdc = ctx->qdc.p;
+  a.qtag = ctx->qtag.p;
+  a.selfpos = ctx->selfpos.as<int32_t>();
+  a.rank = ctx->rank.as<int32_t>();
+  a.order = mode == MODE_ALL ? nullptr : items;
   a.pos_own = ctx->pos_own.p;
   for (int k = 0; k < 3; ++k) a.cellk[k] = cellk ? cellk[k] : nullptr;
   a.cell_of = cell_of;
@@ -303,9 +308,16 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
   a.counts = ctx->counts.as<int32_t>();
   a.masks = ctx->masks.as<unsigned>();
   a.block_sum = ctx->block_sum.as<long long>();
+
+  if (ctx->timing) CK(cudaEventRecord(ctx->ev[0], st));
+  ctx->launches += launch_encode(g.dim, prec, mode, n, C, a.g.counts[0], a.g.wrap[0], a.c, src,
+                                 items, start, ctx->pos_csr.p, ctx->cell_slot.as<int32_t>(), a,
+                                 st);
+  CKL();
+  if (ctx->timing) CK(cudaEventRecord(ctx->ev[1], st));
   launch_count(g.dim, prec, mode, a, st);
   CKL();
-  ctx->launches += 2;
+  ctx->launches += 3;
   return SPHX_OK;
 }
 
@@ -486,7 +498,8 @@ void sphx_destroy(sphx_context* ctx) {
   cudaStreamSynchronize(ctx->stream);
   Buf* all[] = {&ctx->in_x[0], &ctx->in_x[1], &ctx->in_x[2], &ctx->in_cell[0], &ctx->in_cell[1],
                 &ctx->in_cell[2], &ctx->in_items, &ctx->in_start, &ctx->in_cellof, &ctx->pos_own,
-                &ctx->tri, &ctx->rec, &ctx->counts, &ctx->block_sum, &ctx->masks, &ctx->t_offsets, &ctx->t_items,
+                &ctx->tri, &ctx->pos_csr, &ctx->cell_slot, &ctx->qx[0], &ctx->qx[1], &ctx->qx[2], &ctx->qdc,
+                &ctx->qtag, &ctx->rank, &ctx->selfpos, &ctx->counts, &ctx->block_sum, &ctx->masks, &ctx->t_offsets, &ctx->t_items,
                 &ctx->b_counts, &ctx->b_slot, &ctx->b_bad, &ctx->b_tiles, &ctx->b_out_cellof,
                 &ctx->b_out_start, &ctx->b_out_items, &ctx->b_rel[0], &ctx->b_rel[1],
                 &ctx->b_rel[2], &ctx->b_cell[0], &ctx->b_cell[1], &ctx->b_cell[2]};

@@ -31,13 +31,19 @@ struct GridConsts {
   int wrap[3];  // periodic(k) && count(k) > 2  (nnps.cpp:223, :364)
 };
 
-// Arguments of the fused sweep kernel.
+// Arguments of the sweep kernels (encode writes the candidate arrays, count and
+// fill read them).
 struct SweepArgs {
   int n;
   GridConsts g;
   PrecConsts c;
-  const int2* tri;            // [C] record run [x, y) of each cell's x-triple
-  const void* rec;            // candidate records (coords + id << 2 | x code), <= 3n
+  int2* tri;                  // [C] chunk run [x, y) of each cell's x-triple
+  void* qx[3];                // [chunks] coordinate quads per axis (x pre-shifted for CLL)
+  void* qdc;                  // [chunks] RCLL x offset quads dc = cx_i - cx_j
+  void* qtag;                 // [chunks] uint4 particle ids (~0 = sentinel)
+  int32_t* selfpos;           // [n] record index of particle i in its own-cell run
+  int32_t* rank;              // [n] CSR slot of particle i (masks are slot-indexed)
+  const int32_t* order;       // CSR slot -> particle (CellGrid::items), null = identity
   const void* pos_own;        // packed coords in particle order
   const int32_t* cellk[3];    // RCLL: RelCoords::cell[k] (particle order)
   const int32_t* cell_of;     // CLL:  CellGrid::cell_of  (particle order)
