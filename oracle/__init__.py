@@ -35,7 +35,7 @@ def build(quiet: bool = True) -> None:
     """Build the checkers (the reference one only where its sources exist)."""
     targets = ["oracle"]
     if os.path.isdir(REFERENCE_SRC):
-        targets.append("ref")
+        targets += ["ref", "dropin"]
     subprocess.run(["make", "-C", HERE, "-j8", *targets], check=True,
                    stdout=subprocess.DEVNULL if quiet else None)
 
@@ -59,6 +59,17 @@ def fnv_hash(offsets: np.ndarray, items: np.ndarray) -> int:
 # Reference library
 # --------------------------------------------------------------------------------------
 _ref = None
+_dropin = None
+DROPIN_SO = os.path.join(HERE, "_ref", "libsphx_dropin.so")
+
+
+def dropin_lib():
+    """The reference library with its nnps.cpp replaced by our drop-in
+    (paper_2401_08586_b200/csrc/host/nnps_cuda.cpp): same ctypes face as ref_lib()."""
+    global _dropin
+    if _dropin is None:
+        _dropin = _bind_ref(C.CDLL(DROPIN_SO))
+    return _dropin
 
 
 def ref_lib():
@@ -66,7 +77,12 @@ def ref_lib():
     if _ref is None:
         if not os.path.exists(REF_SO):
             build()
-        lib = C.CDLL(REF_SO)
+        _ref = _bind_ref(C.CDLL(REF_SO))
+    return _ref
+
+
+def _bind_ref(lib):
+    if True:
         vp = C.c_void_p
         d3 = C.POINTER(C.c_double)
         sig = {
@@ -117,8 +133,7 @@ def ref_lib():
             f = getattr(lib, name)
             f.restype = res
             f.argtypes = args
-        _ref = lib
-    return _ref
+    return lib
 
 
 def _d3(v):
@@ -147,8 +162,8 @@ class Table:
         return fnv_hash(self.offsets, self.items)
 
 
-def _ref_table(ptr) -> Table:
-    lib = ref_lib()
+def _ref_table(ptr, lib=None) -> Table:
+    lib = lib or ref_lib()
     if not ptr:
         raise RefError(lib.ref_last_error().decode())
     n = lib.ref_table_size(ptr)
@@ -164,34 +179,34 @@ def _ref_table(ptr) -> Table:
 class RefSystem:
     """A reference ParticleSystem + CellGrid + RelCoords triple."""
 
-    def __init__(self, ps_ptr, dim: int):
+    def __init__(self, ps_ptr, dim: int, lib=None):
+        self.lib = lib or ref_lib()
         if not ps_ptr:
-            raise RefError(ref_lib().ref_last_error().decode())
-        self.lib = ref_lib()
+            raise RefError(self.lib.ref_last_error().decode())
         self.ps = ps_ptr
         self.dim = dim
         self.grid = None
         self.rel = None
 
-    # constructors -----------------------------------------------------------------
+    # constructors (lib=dropin_lib() drives the reference with our NNPS) -----------
     @classmethod
-    def lattice(cls, dim, ds, jitter, seed, lo=(0, 0, 0), hi=(1, 1, 1)):
-        lib = ref_lib()
-        return cls(lib.ref_ps_lattice(dim, _d3(lo), _d3(hi), ds, jitter, seed), dim)
+    def lattice(cls, dim, ds, jitter, seed, lo=(0, 0, 0), hi=(1, 1, 1), lib=None):
+        lib = lib or ref_lib()
+        return cls(lib.ref_ps_lattice(dim, _d3(lo), _d3(hi), ds, jitter, seed), dim, lib)
 
     @classmethod
-    def random(cls, dim, n, seed, lo=(0, 0, 0), hi=(1, 1, 1)):
-        lib = ref_lib()
-        return cls(lib.ref_ps_random(dim, _d3(lo), _d3(hi), n, seed), dim)
+    def random(cls, dim, n, seed, lo=(0, 0, 0), hi=(1, 1, 1), lib=None):
+        lib = lib or ref_lib()
+        return cls(lib.ref_ps_random(dim, _d3(lo), _d3(hi), n, seed), dim, lib)
 
     @classmethod
-    def from_arrays(cls, x, ds, lo=(0, 0, 0), hi=(1, 1, 1), h=None):
-        lib = ref_lib()
+    def from_arrays(cls, x, ds, lo=(0, 0, 0), hi=(1, 1, 1), h=None, lib=None):
+        lib = lib or ref_lib()
         dim = len(x)
         xs = [np.ascontiguousarray(a, np.float64) for a in x]
         ptrs = [a.ctypes.data for a in xs] + [None] * (3 - dim)
         n = len(xs[0])
-        self = cls(lib.ref_ps_from_arrays(dim, _d3(lo), _d3(hi), ds, n, *ptrs), dim)
+        self = cls(lib.ref_ps_from_arrays(dim, _d3(lo), _d3(hi), ds, n, *ptrs), dim, lib)
         if h is not None:
             lib.ref_ps_set_h(self.ps, h)
         return self
@@ -287,13 +302,13 @@ class RefSystem:
 
     # backends ----------------------------------------------------------------------
     def rcll(self, prec) -> Table:
-        return _ref_table(self.lib.ref_rcll(self.rel, self.grid, prec))
+        return _ref_table(self.lib.ref_rcll(self.rel, self.grid, prec), self.lib)
 
     def cll(self, prec) -> Table:
-        return _ref_table(self.lib.ref_cll(self.ps, self.grid, prec))
+        return _ref_table(self.lib.ref_cll(self.ps, self.grid, prec), self.lib)
 
     def all_list(self, prec) -> Table:
-        return _ref_table(self.lib.ref_all_list(self.ps, prec))
+        return _ref_table(self.lib.ref_all_list(self.ps, prec), self.lib)
 
     def time_nnps(self, backend: str, prec: int, repeats: int = 5) -> float:
         which = 0 if backend == "rcll" else 1

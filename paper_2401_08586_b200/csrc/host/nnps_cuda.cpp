@@ -1,0 +1,173 @@
+// Drop-in implementation of the reference's NNPS interface (nnps.hpp) on the
+// B200: the three backends call the C ABI of libsphx_cuda.so, which runs the
+// sm_100a kernels; nothing here computes a neighbour decision.
+//
+// This file uses only the public interface of sphx/nnps.hpp, cell_grid.hpp and
+// particle_system.hpp (plus the ParticleSystem friend apply_permutation, as the
+// reference declares it), so it compiles unchanged against the reference's own
+// headers: replacing the reference's src/nnps.cpp with this file and linking
+// libsphx_cuda.so is the whole integration.
+
+#include <algorithm>
+#include <numeric>
+#include <stdexcept>
+
+#include "session.hpp"
+#include "sphx/nnps.hpp"
+#include "sphx_cuda.h"
+
+namespace sphx {
+
+namespace {
+
+int32_t prec_code(Precision p) {
+  return p == Precision::fp64 ? SPHX_FP64 : (p == Precision::fp32 ? SPHX_FP32 : SPHX_FP16);
+}
+
+NeighborTable take_table(sphx_context* ctx, std::size_t n, std::int64_t total, double radius) {
+  NeighborTable t;
+  t.radius = radius;
+  t.offsets.resize(n + 1);
+  t.items.resize(static_cast<std::size_t>(total));
+  cuda::check(sphx_table_copy(ctx, t.offsets.data(), t.items.empty() ? nullptr : t.items.data()));
+  return t;
+}
+
+}  // namespace
+
+// nnps.hpp:31 (reference nnps.cpp:128-172)
+NeighborTable all_list(const ParticleSystem& ps, Precision prec) {
+  const std::size_t n = ps.size();
+  if (n == 0) throw std::invalid_argument("all_list needs at least one particle");
+  const double* x[3] = {nullptr, nullptr, nullptr};
+  for (int k = 0; k < ps.dim(); ++k) x[k] = ps.x(k).data();
+  sphx_context* ctx = cuda::context();
+  std::int64_t total = 0;
+  cuda::check(sphx_all_list(ctx, ps.dim(), static_cast<std::int64_t>(n), x, ps.h(),
+                            prec_code(prec), &total));
+  return take_table(ctx, n, total, 2.0 * ps.h());
+}
+
+// nnps.hpp:36 (reference nnps.cpp:174-281)
+NeighborTable cell_link_list(const ParticleSystem& ps, const CellGrid& grid, Precision prec) {
+  const std::size_t n = ps.size();
+  const auto items = grid.items();
+  if (items.size() != n) throw std::invalid_argument("grid membership is stale; rebin first");
+  std::vector<std::int32_t> cell_of(n);
+  for (std::size_t i = 0; i < n; ++i) cell_of[i] = grid.cell_of(i);
+  const double* x[3] = {nullptr, nullptr, nullptr};
+  for (int k = 0; k < ps.dim(); ++k) x[k] = ps.x(k).data();
+  const sphx_grid_desc g = cuda::describe(grid);
+  sphx_context* ctx = cuda::context();
+  std::int64_t total = 0;
+  cuda::check(sphx_cell_link_list(ctx, &g, static_cast<std::int64_t>(n), x, ps.h(),
+                                  static_cast<std::int64_t>(items.size()), items.data(),
+                                  grid.cell_start().data(), cell_of.data(), prec_code(prec),
+                                  &total));
+  return take_table(ctx, n, total, 2.0 * ps.h());
+}
+
+// nnps.hpp:41 (reference nnps.cpp:283-416)
+NeighborTable rcll(const RelCoords& rc, const CellGrid& grid, Precision prec) {
+  const std::size_t n = rc.size();
+  const auto items = grid.items();
+  if (items.size() != n) throw std::invalid_argument("grid membership is stale");
+  const double* rel[3] = {nullptr, nullptr, nullptr};
+  const std::int32_t* cell[3] = {nullptr, nullptr, nullptr};
+  for (int k = 0; k < grid.dim(); ++k) {
+    rel[k] = rc.rel[k].data();
+    cell[k] = rc.cell[k].data();
+  }
+  const sphx_grid_desc g = cuda::describe(grid);
+  sphx_context* ctx = cuda::context();
+  std::int64_t total = 0;
+  cuda::check(sphx_rcll(ctx, &g, static_cast<std::int64_t>(n), rel, cell,
+                        static_cast<std::int64_t>(items.size()), items.data(),
+                        grid.cell_start().data(), prec_code(prec), &total));
+  return take_table(ctx, n, total, grid.radius_phys());
+}
+
+// ---- table utilities (host; not on the search path) -------------------------------
+
+MismatchReport mismatch_report(const NeighborTable& candidate, const NeighborTable& oracle) {
+  if (candidate.size() != oracle.size())
+    throw std::invalid_argument("tables cover different particle counts");
+  MismatchReport rep;
+  for (std::size_t i = 0; i < oracle.size(); ++i) {
+    const auto a = candidate.row(i);
+    const auto b = oracle.row(i);
+    // directed symmetric difference of two ascending rows
+    std::size_t p = 0, q = 0;
+    while (p < a.size() && q < b.size()) {
+      if (a[p] == b[q]) {
+        ++p;
+        ++q;
+      } else {
+        ++rep.incorrect_count;
+        (a[p] < b[q] ? p : q) += 1;
+      }
+    }
+    rep.incorrect_count += (a.size() - p) + (b.size() - q);
+  }
+  const double denom = static_cast<double>(oracle.total());
+  rep.incorrect_percent = denom > 0.0 ? 100.0 * static_cast<double>(rep.incorrect_count) / denom : 0.0;
+  return rep;
+}
+
+std::vector<std::uint32_t> spatial_sort_permutation(const ParticleSystem& ps) {
+  std::vector<std::uint32_t> perm(ps.size());
+  std::iota(perm.begin(), perm.end(), 0u);
+  const int dim = ps.dim();
+  std::stable_sort(perm.begin(), perm.end(), [&](std::uint32_t a, std::uint32_t b) {
+    for (int k = 0; k < dim; ++k) {
+      const double xa = ps.x(k)[a], xb = ps.x(k)[b];
+      if (xa != xb) return xa < xb;
+    }
+    return a < b;
+  });
+  return perm;
+}
+
+void apply_permutation(ParticleSystem& ps, const std::vector<std::uint32_t>& perm) {
+  const std::size_t n = ps.size();
+  if (perm.size() != n) throw std::invalid_argument("permutation size mismatch");
+  auto gather = [&](std::vector<double>& a) {
+    if (a.size() != n) return;
+    std::vector<double> out(n);
+    for (std::size_t q = 0; q < n; ++q) out[q] = a[perm[q]];
+    a.swap(out);
+  };
+  for (int k = 0; k < ps.dim(); ++k) {
+    gather(ps.x_[k]);
+    gather(ps.v_[k]);
+  }
+  gather(ps.rho_);
+  gather(ps.p_);
+  gather(ps.e_);
+  gather(ps.m_);
+}
+
+NeighborTable remap_table(const NeighborTable& t, const std::vector<std::uint32_t>& perm) {
+  const std::size_t n = t.size();
+  std::vector<std::uint32_t> inv(n);
+  for (std::size_t q = 0; q < n; ++q) inv[perm[q]] = static_cast<std::uint32_t>(q);
+  NeighborTable out;
+  out.radius = t.radius;
+  out.offsets.assign(n + 1, 0);
+  for (std::size_t q = 0; q < n; ++q)
+    out.offsets[q + 1] = out.offsets[q] + static_cast<std::int64_t>(t.row(perm[q]).size());
+  out.items.resize(static_cast<std::size_t>(out.offsets[n]));
+  for (std::size_t q = 0; q < n; ++q) {
+    const auto src = t.row(perm[q]);
+    std::int32_t* dst = out.items.data() + out.offsets[q];
+    for (std::size_t e = 0; e < src.size(); ++e) dst[e] = static_cast<std::int32_t>(inv[src[e]]);
+    std::sort(dst, dst + src.size());
+  }
+  return out;
+}
+
+bool tables_equal(const NeighborTable& a, const NeighborTable& b) {
+  return a.size() == b.size() && a.offsets == b.offsets && a.items == b.items;
+}
+
+}  // namespace sphx
