@@ -228,7 +228,8 @@ def run_ours(args):
     world, rank, local = dist_env()
     if world > 1:
         from paper_2401_08586_b200 import multigpu
-        return multigpu.bench(args, WORKLOADS, METRIC)
+        return multigpu.bench(args, WORKLOADS, METRIC, clock_sampler=ClockSampler,
+                              peaks=measured_peaks())
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)

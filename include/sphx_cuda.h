@@ -165,6 +165,37 @@ int sphx_rebin_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
                       const double* const d_x[3], int32_t* d_cell_of, int32_t* d_cell_start,
                       int32_t* d_items, int64_t* d_bad);
 
+/* ---------------- slab decomposition (one process per GPU) ----------------
+ * No reference counterpart: the reference is single-process.
+ * A rank owns the cell layers [L0, L1) of the global grid along `axis` (the
+ * slowest axis) plus one halo layer on each side received from its neighbours.
+ * Its local grid is the global grid with counts[axis] = L1 - L0 + 2 and
+ * periodic[axis] = 0; local layer l is global layer (L0 - 1 + l) mod G. */
+
+/* build_rel_coords on the slab: each particle is located on the GLOBAL grid
+ * (global normalisation, rel and cell choice bit-identical to the one-GPU run),
+ * then its `axis` layer becomes (c - layer0) mod G and CSR is built over `local`. */
+int sphx_build_rel_coords_window_device(sphx_context* ctx, const sphx_grid_desc* global,
+                                        const sphx_grid_desc* local, int32_t axis,
+                                        int32_t layer0, int64_t n, const double* const d_x[3],
+                                        double* const d_rel[3], int32_t* const d_cell[3],
+                                        int32_t* d_cell_of, int32_t* d_cell_start,
+                                        int32_t* d_items);
+
+/* RCLL rows for particles [row0, row0 + nrows) only (the owned particles of a
+ * slab); neighbour ids are written as d_ids[j] (global ids; NULL = local j).
+ * d_offsets has nrows + 1 entries; d_offsets[nrows] = exact total. */
+int sphx_rcll_rows_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                          const double* const d_rel[3], const int32_t* const d_cell[3],
+                          const int32_t* d_items, const int32_t* d_cell_start, int32_t precision,
+                          const int32_t* d_ids, int64_t row0, int64_t nrows, int64_t* d_offsets,
+                          int32_t* d_items_out, int64_t capacity);
+
+/* Un-jittered build_lattice sites with ids [id0, id0 + count) written to d_x
+ * (x_k = lo_k + (c_k + 0.5) ds, bit-identical to particle_system.cpp:53). */
+int sphx_lattice_device(sphx_context* ctx, int32_t dim, const double lo[3], const double hi[3],
+                        double ds, int64_t id0, int64_t count, double* const d_x[3]);
+
 /* ---------------- synthetic inputs ---------------- */
 
 /* build_lattice(Domain::box(dim, lo, hi), ds, jitter, seed) (particle_system.hpp:66,

@@ -86,6 +86,12 @@ def lib():
                                                 C.c_uint64, C.POINTER(dbl), vp, vp, vp]),
         "sphx_last_timing": (C.c_int, [vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
         "sphx_table_hash": (C.c_uint64, [vp, i64, vp, i64]),
+        "sphx_build_rel_coords_window_device": (C.c_int, [vp, G, G, i32, i32, i64, p3, p3, p3,
+                                                          vp, vp, vp]),
+        "sphx_rcll_rows_device": (C.c_int, [vp, G, i64, p3, p3, vp, vp, i32, vp, i64, i64, vp,
+                                            vp, i64]),
+        "sphx_lattice_device": (C.c_int, [vp, i32, C.POINTER(dbl), C.POINTER(dbl), dbl, i64, i64,
+                                          p3]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -101,7 +107,8 @@ EXPORTED = ("sphx_last_error", "sphx_grid_init", "sphx_create", "sphx_destroy",
             "sphx_rebuild_members", "sphx_rcll_device", "sphx_cell_link_list_device",
             "sphx_build_rel_coords_device", "sphx_rebin_device", "sphx_enable_timing",
             "sphx_last_timing", "sphx_build_lattice", "sphx_build_random_uniform",
-            "sphx_table_hash")
+            "sphx_table_hash", "sphx_build_rel_coords_window_device", "sphx_rcll_rows_device",
+            "sphx_lattice_device")
 
 
 def table_hash(offsets: np.ndarray, items: np.ndarray) -> int:
@@ -311,3 +318,22 @@ class Context:
         check(lib().sphx_build_rel_coords_device(self.h, C.byref(grid), x[0].numel(), _dptr3(x),
                                                  _dptr3(rel), _dptr3(cell), cell_of.data_ptr(),
                                                  cell_start.data_ptr(), items.data_ptr()))
+
+    # ---- slab decomposition (multigpu.py) -----------------------------------------------
+    def build_rel_coords_window_device(self, global_grid, local_grid, axis, layer0, x, rel, cell,
+                                       cell_of, cell_start, items):
+        check(lib().sphx_build_rel_coords_window_device(
+            self.h, C.byref(global_grid), C.byref(local_grid), axis, layer0, x[0].numel(),
+            _dptr3(x), _dptr3(rel), _dptr3(cell), cell_of.data_ptr(), cell_start.data_ptr(),
+            items.data_ptr()))
+
+    def rcll_rows_device(self, grid, rel, cell, items, cell_start, prec, ids, row0, nrows,
+                         offsets, items_out):
+        check(lib().sphx_rcll_rows_device(
+            self.h, C.byref(grid), rel[0].numel(), _dptr3(rel), _dptr3(cell), items.data_ptr(),
+            cell_start.data_ptr(), prec, ids.data_ptr() if ids is not None else None, row0, nrows,
+            offsets.data_ptr(), items_out.data_ptr(), items_out.numel()))
+
+    def lattice_device(self, dim, lo, hi, ds, id0, x):
+        check(lib().sphx_lattice_device(self.h, dim, _d3(lo), _d3(hi), float(ds), id0,
+                                        x[0].numel(), _dptr3(x)))

@@ -41,12 +41,12 @@ __device__ __forceinline__ void locate_axis(const BinConsts& g, int k, double xn
   const double off = __dsub_rn(xn, g.origin[k]);
   int c = x86_cvt_i32(floor(__ddiv_rn(off, g.hc[k])));
   if (c < 0) c = 0;
-  if (c >= g.counts[k]) c = g.counts[k] - 1;
+  if (c >= g.loc_counts[k]) c = g.loc_counts[k] - 1;
   double r = __ddiv_rn(__dmul_rn(2.0, __dsub_rn(xn, center_norm(g, k, c))), g.hc[k]);
   if (r < -1.0 && c > 0) {
     --c;
     r = __ddiv_rn(__dmul_rn(2.0, __dsub_rn(xn, center_norm(g, k, c))), g.hc[k]);
-  } else if (r > 1.0 && c + 1 < g.counts[k]) {
+  } else if (r > 1.0 && c + 1 < g.loc_counts[k]) {
     ++c;
     r = __ddiv_rn(__dmul_rn(2.0, __dsub_rn(xn, center_norm(g, k, c))), g.hc[k]);
   }
@@ -73,12 +73,16 @@ __global__ void k_locate(LocateArgs a) {
           __ddiv_rn(__dsub_rn(__dmul_rn(2.0, a.x[k][i]), __dadd_rn(g.hi[k], g.lo[k])), g.hd);
       if (MODE == BIN_REBIN) {
         const double off = __dsub_rn(xn, g.origin[k]);
-        const double top = __dmul_rn((double)g.counts[k], g.hc[k]);
+        const double top = __dmul_rn((double)g.loc_counts[k], g.hc[k]);
         if (off < __dmul_rn(-1e-9, g.hc[k]) || off > __dadd_rn(top, __dmul_rn(1e-9, g.hc[k])))
           outside = true;
       }
       double r;
       locate_axis(g, k, xn, c[k], r);
+      if (k == g.win_axis) {  // global layer -> slab-local layer (periodic wrap)
+        c[k] = (c[k] - g.win_lo + g.win_global) % g.win_global;
+        if (c[k] >= g.counts[k]) c[k] = g.counts[k] - 1;  // outside the window: malformed
+      }
       if (MODE == BIN_REL) {
         a.rel_out[k][i] = r;
         a.cell_out[k][i] = c[k];
@@ -162,6 +166,28 @@ __global__ void k_cell_sort(int64_t C, const int32_t* __restrict__ start, int32_
   }
 }
 
+// Un-jittered lattice sites [id0, id0 + count) of build_lattice
+// (particle_system.cpp:49-56): x_k = lo_k + (c_k + 0.5) * ds, x fastest.
+// Lets each rank of a slab run create its own slab of a lattice directly in HBM.
+struct LatticeArgs {
+  int dim;
+  double lo[3], ds;
+  long long counts[3];
+  long long id0, count;
+  double* x[3];
+};
+
+__global__ void k_lattice(LatticeArgs a) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= a.count) return;
+  long long id = a.id0 + t;
+  for (int k = 0; k < a.dim; ++k) {
+    const long long c = id % a.counts[k];
+    id /= a.counts[k];
+    a.x[k][t] = __dadd_rn(a.lo[k], __dmul_rn(__dadd_rn((double)c, 0.5), a.ds));
+  }
+}
+
 // ------------------------------------------------------------------------------
 // Host launchers
 // ------------------------------------------------------------------------------
@@ -187,6 +213,21 @@ void launch_scatter_sort(int n, int64_t C, const int32_t* cell_of, const int32_t
                          const int32_t* start, int32_t* items, cudaStream_t st) {
   if (n > 0) k_scatter<<<(n + 255) / 256, 256, 0, st>>>(n, cell_of, slot, start, items);
   if (C > 0) k_cell_sort<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(C, start, items);
+}
+
+void launch_lattice(int dim, const double lo[3], double ds, const int64_t counts[3], int64_t id0,
+                    int64_t count, double* const x[3], cudaStream_t st) {
+  LatticeArgs a;
+  a.dim = dim;
+  a.ds = ds;
+  a.id0 = id0;
+  a.count = count;
+  for (int k = 0; k < 3; ++k) {
+    a.lo[k] = k < dim ? lo[k] : 0.0;
+    a.counts[k] = counts[k];
+    a.x[k] = k < dim ? x[k] : nullptr;
+  }
+  k_lattice<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(a);
 }
 
 }  // namespace sphx_dev

@@ -35,6 +35,8 @@ void launch_scan_counts(const int32_t* in, int32_t* out, int64_t C, unsigned lon
                         int* counter, cudaStream_t st);
 void launch_scatter_sort(int n, int64_t C, const int32_t* cell_of, const int32_t* slot,
                          const int32_t* start, int32_t* items, cudaStream_t st);
+void launch_lattice(int dim, const double lo[3], double ds, const int64_t counts[3], int64_t id0,
+                    int64_t count, double* const x[3], cudaStream_t st);
 }  // namespace sphx_dev
 
 using namespace sphx_dev;
@@ -242,11 +244,26 @@ BinConsts bin_consts(const sphx_grid_desc& g) {
   b.hd = hd;
   for (int k = 0; k < 3; ++k) {
     b.counts[k] = k < g.dim ? g.counts[k] : 1;
+    b.loc_counts[k] = b.counts[k];
     b.hc[k] = g.hc[k];
     b.origin[k] = g.origin[k];
     b.lo[k] = g.lo[k];
     b.hi[k] = g.hi[k];
   }
+  b.win_axis = -1;
+  return b;
+}
+
+// Slab window: locate on the global grid (its normalisation, origin and
+// counts), keep layers [layer0, layer0 + local.counts[axis]) (mod the global
+// count) along `axis`, CSR over the local grid.
+BinConsts window_consts(const sphx_grid_desc& global, const sphx_grid_desc& local, int axis,
+                        int layer0) {
+  BinConsts b = bin_consts(global);
+  for (int k = 0; k < 3; ++k) b.counts[k] = k < local.dim ? local.counts[k] : 1;
+  b.win_axis = axis;
+  b.win_lo = layer0;
+  b.win_global = global.counts[axis];
   return b;
 }
 
@@ -259,23 +276,37 @@ int upload(sphx_context* ctx, Buf& b, const void* src, size_t bytes) {
 // Encode + count + block-sum scan on device pointers (src = rel for RCLL,
 // positions for CLL/ALL). Leaves the exact total in d_off[n] and the sweep
 // arguments in *out for the fill pass.
+// Rows to produce: particles [row0, row0 + nrows); ids = output id of each
+// particle (null: its index). The multi-GPU slab path asks for the owned rows
+// of a slab-local system with global ids.
+struct RowSel {
+  int64_t row0 = 0, nrows = -1;  // nrows < 0: all
+  const int32_t* ids = nullptr;
+};
+
 int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n64,
                 const double* const src[3], const int32_t* const cellk[3], const int32_t* items,
                 const int32_t* start, const int32_t* cell_of, int prec, double h, int64_t* d_off,
-                SweepArgs* out) {
+                SweepArgs* out, const RowSel& sel = RowSel()) {
   if (n64 > INT32_MAX - 64)
     return fail(SPHX_ERR_INVALID_ARGUMENT, "too many particles for one context (int32 ids)");
   const int n = (int)n64;
+  const int64_t nrows = sel.nrows < 0 ? n64 : sel.nrows;
+  if (sel.row0 < 0 || sel.row0 + nrows > n64)
+    return fail(SPHX_ERR_INVALID_ARGUMENT, "row range outside the system");
   cudaStream_t st = ctx->stream;
   std::memset(out, 0, sizeof(*out));
   out->n = n;
-  if (n == 0) {
+  out->row0 = (int)sel.row0;
+  out->nrows = (int)nrows;
+  out->ids = sel.ids;
+  if (n == 0 || nrows == 0) {
     CK(cudaMemsetAsync(d_off, 0, sizeof(int64_t), st));
     return SPHX_OK;
   }
   const int64_t C = mode == MODE_ALL ? 0 : cell_total(g);
   const int64_t chunks = chunk_capacity(mode, n, C);
-  const int nb = (n + fill_tile(g.dim) - 1) / fill_tile(g.dim);
+  const int nb = (int)((nrows + fill_tile(g.dim) - 1) / fill_tile(g.dim));
   TRY(ctx->pos_own.ensure(coord_bytes(g.dim, prec) * (size_t)n));
   for (int k = 0; k < g.dim; ++k) TRY(ctx->qx[k].ensure(quad_bytes(prec) * (size_t)chunks));
   TRY(ctx->qtag.ensure(16 * (size_t)chunks));
@@ -323,7 +354,7 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
 
 int run_fill(sphx_context* ctx, int mode, int dim, int prec, SweepArgs& a, int32_t* d_items,
              int64_t capacity) {
-  if (a.n == 0) return SPHX_OK;
+  if (a.n == 0 || a.nrows == 0) return SPHX_OK;
   a.items = d_items;
   a.capacity = capacity;
   launch_fill(dim, prec, mode, a, ctx->stream);
@@ -378,7 +409,8 @@ int check_ctx(sphx_context* ctx) {
 int run_binning(sphx_context* ctx, int bmode, const sphx_grid_desc& g, int64_t n64,
                 const double* const d_x[3], const int32_t* const d_cell_in[3],
                 double* const d_rel[3], int32_t* const d_cell[3], int32_t* d_cell_of,
-                int32_t* d_start, int32_t* d_items, unsigned long long* d_bad) {
+                int32_t* d_start, int32_t* d_items, unsigned long long* d_bad,
+                const BinConsts* window = nullptr) {
   const int n = (int)n64;
   const int64_t C = cell_total(g);
   cudaStream_t st = ctx->stream;
@@ -391,7 +423,7 @@ int run_binning(sphx_context* ctx, int bmode, const sphx_grid_desc& g, int64_t n
   LocateArgs a;
   std::memset(&a, 0, sizeof(a));
   a.n = n;
-  a.g = bin_consts(g);
+  a.g = window ? *window : bin_consts(g);
   for (int k = 0; k < 3; ++k) {
     a.x[k] = d_x ? d_x[k] : nullptr;
     a.cell_in[k] = d_cell_in ? d_cell_in[k] : nullptr;
@@ -739,6 +771,65 @@ int sphx_rebin_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
   CK(cudaMemsetAsync(d_bad, 0xFF, sizeof(int64_t), ctx->stream));
   return run_binning(ctx, 0, *grid, n, d_x, nullptr, nullptr, nullptr, d_cell_of, d_cell_start,
                      d_items, reinterpret_cast<unsigned long long*>(d_bad));
+}
+
+// ---------------- multi-GPU slab path ----------------
+
+int sphx_rcll_rows_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                          const double* const d_rel[3], const int32_t* const d_cell[3],
+                          const int32_t* d_items, const int32_t* d_cell_start, int32_t precision,
+                          const int32_t* d_ids, int64_t row0, int64_t nrows, int64_t* d_offsets,
+                          int32_t* d_items_out, int64_t capacity) {
+  TRY(check_ctx(ctx));
+  if (!grid) return fail(SPHX_ERR_INVALID_ARGUMENT, "null grid");
+  TRY(check_prec_dim(precision, grid->dim));
+  RowSel sel;
+  sel.row0 = row0;
+  sel.nrows = nrows;
+  sel.ids = d_ids;
+  SweepArgs a;
+  TRY(run_prepare(ctx, MODE_RCLL, *grid, n, d_rel, d_cell, d_items, d_cell_start, nullptr,
+                  precision, 0.0, d_offsets, &a, sel));
+  return run_fill(ctx, MODE_RCLL, grid->dim, precision, a, d_items_out, capacity);
+}
+
+int sphx_build_rel_coords_window_device(sphx_context* ctx, const sphx_grid_desc* global,
+                                        const sphx_grid_desc* local, int32_t axis, int32_t layer0,
+                                        int64_t n, const double* const d_x[3],
+                                        double* const d_rel[3], int32_t* const d_cell[3],
+                                        int32_t* d_cell_of, int32_t* d_cell_start,
+                                        int32_t* d_items) {
+  TRY(check_ctx(ctx));
+  if (!global || !local) return fail(SPHX_ERR_INVALID_ARGUMENT, "null grid");
+  TRY(check_prec_dim(SPHX_FP64, global->dim));
+  if (axis < 0 || axis >= global->dim || local->dim != global->dim)
+    return fail(SPHX_ERR_INVALID_ARGUMENT, "bad slab window");
+  for (int k = 0; k < global->dim; ++k)
+    if (k != axis && local->counts[k] != global->counts[k])
+      return fail(SPHX_ERR_INVALID_ARGUMENT, "slab grid differs from the global grid off the slab axis");
+  if (local->counts[axis] < 1 || local->counts[axis] > global->counts[axis] + 2 || layer0 < -1 ||
+      layer0 >= global->counts[axis])
+    return fail(SPHX_ERR_INVALID_ARGUMENT, "slab window outside the global grid");
+  TRY(ctx->b_bad.ensure(sizeof(unsigned long long)));
+  const BinConsts w = window_consts(*global, *local, axis, layer0);
+  return run_binning(ctx, 1, *local, n, d_x, nullptr, d_rel, d_cell, d_cell_of, d_cell_start,
+                     d_items, ctx->b_bad.as<unsigned long long>(), &w);
+}
+
+int sphx_lattice_device(sphx_context* ctx, int32_t dim, const double lo[3], const double hi[3],
+                        double ds, int64_t id0, int64_t count, double* const d_x[3]) {
+  TRY(check_ctx(ctx));
+  TRY(check_prec_dim(SPHX_FP64, dim));
+  int64_t counts[3] = {1, 1, 1};
+  for (int k = 0; k < dim; ++k) counts[k] = static_cast<int64_t>(std::floor((hi[k] - lo[k]) / ds + 0.5));
+  const int64_t total = counts[0] * counts[1] * counts[2];
+  if (id0 < 0 || count < 0 || id0 + count > total)
+    return fail(SPHX_ERR_INVALID_ARGUMENT, "lattice id range outside the lattice");
+  if (count == 0) return SPHX_OK;
+  launch_lattice(dim, lo, ds, counts, id0, count, d_x, ctx->stream);
+  CKL();
+  ++ctx->launches;
+  return SPHX_OK;
 }
 
 // ---------------- synthetic inputs (particle_system.cpp:31-77) ----------------

@@ -50,6 +50,8 @@ struct SweepArgs {
   int64_t* offsets;           // [n+1]
   int32_t* items;             // [capacity]
   int64_t capacity;
+  int row0, nrows;            // rows produced: particles [row0, row0 + nrows)
+  const int32_t* ids;         // output id of particle j (null: j) -- global ids of a slab
   int32_t* counts;            // [n] row lengths (pass 1), bit 31: masks overflowed
   unsigned* masks;            // [W][n] hit nibbles of every 4-record chunk (pass 1)
   long long* block_sum;       // [blocks] row-length sums, scanned in place (pass 2)
@@ -126,9 +128,14 @@ __device__ __forceinline__ long long lookback_exclusive(unsigned long long* tile
 // Binning (binning.cu)
 struct BinConsts {
   int dim;
-  int counts[3];
+  int counts[3];  // cell counts of the (local) CSR grid
   double hc[3], origin[3], lo[3], hi[3];
   double hd;
+  // slab window (multi-GPU): cells are located on the global grid, then the
+  // window axis coordinate becomes (c - win_lo) mod win_global
+  int win_axis;  // -1: no window
+  int win_lo, win_global;
+  int loc_counts[3];  // counts used by locate (global grid)
 };
 
 struct LocateArgs {

@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(BT) k_count(SweepArgs a) {
   const int s = blockIdx.x * BT + threadIdx.x;
   if (s >= a.n) return;
   const int i = a.order ? __ldg(a.order + s) : s;
-  if (i < 0 || i >= a.n) return;  // malformed membership
+  if (i < a.row0 || i >= a.row0 + a.nrows) return;  // not a requested row (or malformed)
   int k = 0, bits = 0, words = 0;
   unsigned acc = 0;
   scan_particle<D, P, MODE>(a, i, [&](unsigned m, int64_t) {
@@ -684,8 +684,10 @@ __global__ void __launch_bounds__(BT) k_fill(SweepArgs a) {
   __shared__ int32_t S[BT * CAP];
   __shared__ int s_w[BT / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int i = blockIdx.x * BT + tid;
-  const unsigned kw = i < a.n ? (unsigned)__ldg(a.counts + i) : 0u;
+  const int r = blockIdx.x * BT + tid;  // row index (particle row0 + r)
+  const bool valid = r < a.nrows;
+  const int i = a.row0 + r;
+  const unsigned kw = valid ? (unsigned)__ldg(a.counts + i) : 0u;
   const int k = (int)(kw & ~kOverflow);
   const bool retest = (kw & kOverflow) != 0u;
   const int incl = warp_inclusive_scan(k);
@@ -700,10 +702,10 @@ __global__ void __launch_bounds__(BT) k_fill(SweepArgs a) {
   }
   const long long bbase = a.block_sum[blockIdx.x];  // scanned in place by pass 2
   const long long grow = bbase + wbase + incl - k;
-  if (i < a.n) a.offsets[i] = grow;
+  if (valid) a.offsets[r] = grow;
   if (bbase + btot > a.capacity) return;  // device API: the caller grows the table
 
-  const int64_t s = MODE == MODE_ALL ? i : (i < a.n ? (int64_t)__ldg(a.rank + i) : 0);
+  const int64_t s = MODE == MODE_ALL ? i : (valid ? (int64_t)__ldg(a.rank + i) : 0);
   const unsigned over = __ballot_sync(0xffffffffu, k > CAP);
   int32_t* wS = S + warp * 32 * CAP;
   int32_t* __restrict__ out = a.items + bbase + wbase;
@@ -731,11 +733,11 @@ __global__ void __launch_bounds__(BT) k_fill(SweepArgs a) {
     }
   }
   __syncwarp();
-  for (int r = 0; r < 32; ++r) {
-    const int len = __shfl_sync(0xffffffffu, k, r);
-    const int ro = __shfl_sync(0xffffffffu, wrel, r);
+  for (int w = 0; w < 32; ++w) {
+    const int len = __shfl_sync(0xffffffffu, k, w);
+    const int ro = __shfl_sync(0xffffffffu, wrel, w);
     if (len > CAP) continue;
-    for (int q = lane; q < len; q += 32) out[ro + q] = wS[r * CAP + q];
+    for (int q = lane; q < len; q += 32) out[ro + q] = wS[w * CAP + q];
   }
 }
 
@@ -905,7 +907,8 @@ __global__ void k_encode_members(int n, int nx, int wrapx, PrecConsts pc,
       store_el<P>(a.qx[k], r, v);
     }
     if constexpr (MODE == MODE_RCLL) store_el<P>(a.qdc, r, (T)(float)(1 - L));  // dc_x
-    reinterpret_cast<unsigned*>(a.qtag)[r] = (unsigned)j;
+    // output id: the particle index, or its global id for a multi-GPU slab
+    reinterpret_cast<unsigned*>(a.qtag)[r] = a.ids ? (unsigned)__ldg(a.ids + j) : (unsigned)j;
     if (L == 1) a.selfpos[j] = (int)r;
   }
 }
@@ -1018,15 +1021,15 @@ static void count_t(const SweepArgs& a, cudaStream_t st) {
   constexpr int CBT = Shape<D>::CBT;
   k_count<D, P, M, CBT><<<(a.n + CBT - 1) / CBT, CBT, 0, st>>>(a);
   const int tile = Shape<D>::BT;
-  const int nt = (a.n + tile - 1) / tile;
-  k_tile_sums<<<nt, 256, 0, st>>>(a.counts, a.n, tile, a.block_sum);
-  k_scan_blocks<<<1, 1024, 0, st>>>(a.block_sum, nt, a.offsets, a.n);
+  const int nt = (a.nrows + tile - 1) / tile;
+  k_tile_sums<<<nt, 256, 0, st>>>(a.counts + a.row0, a.nrows, tile, a.block_sum);
+  k_scan_blocks<<<1, 1024, 0, st>>>(a.block_sum, nt, a.offsets, a.nrows);
 }
 
 template <int D, int P, int M>
 static void fill_t(const SweepArgs& a, cudaStream_t st) {
   constexpr int BT = Shape<D>::BT;
-  k_fill<D, P, M, BT, Shape<D>::CAP><<<(a.n + BT - 1) / BT, BT, 0, st>>>(a);
+  k_fill<D, P, M, BT, Shape<D>::CAP><<<(a.nrows + BT - 1) / BT, BT, 0, st>>>(a);
 }
 
 #define SW(FN, D, P, M) \
