@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--precision", default="fp16", choices=sorted(PREC))
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--slab", action="store_true",
+                    help="use the slab-decomposed (multi-GPU) path even at N=1")
     return ap.parse_args()
 
 
@@ -226,7 +228,7 @@ def run_ours(args):
     import paper_2401_08586_b200 as P
 
     world, rank, local = dist_env()
-    if world > 1:
+    if world > 1 or args.slab:
         from paper_2401_08586_b200 import multigpu
         return multigpu.bench(args, WORKLOADS, METRIC, clock_sampler=ClockSampler,
                               peaks=measured_peaks())

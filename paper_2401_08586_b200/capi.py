@@ -208,7 +208,20 @@ class Context:
         return int(lib().sphx_launch_count(self.h))
 
     def set_stream(self, stream_handle: int | None):
+        """Pin the context to a CUDA stream (None: back to following torch)."""
         check(lib().sphx_set_stream(self.h, stream_handle))
+        self._pinned = stream_handle is not None
+
+    def _bind(self, t):
+        """Device API calls are ordered on torch's current stream of the tensors'
+        device unless a stream was pinned with set_stream()."""
+        if getattr(self, "_pinned", False):
+            return
+        import torch
+        # torch's default stream has handle 0, which the ABI reads as "own stream":
+        # pass cudaStreamLegacy (0x1) for it instead
+        h = torch.cuda.current_stream(t.device).cuda_stream or 0x1
+        check(lib().sphx_set_stream(self.h, h))
 
     def enable_timing(self, on: bool = True):
         check(lib().sphx_enable_timing(self.h, int(on)))
@@ -303,18 +316,21 @@ class Context:
 
     # ---- device-resident API (torch tensors as device memory) ---------------------------
     def rcll_device(self, grid, rel, cell, items, cell_start, prec, offsets, items_out):
+        self._bind(offsets)
         check(lib().sphx_rcll_device(self.h, C.byref(grid), rel[0].numel(), _dptr3(rel),
                                      _dptr3(cell), items.data_ptr(), cell_start.data_ptr(), prec,
                                      offsets.data_ptr(), items_out.data_ptr(), items_out.numel()))
 
     def cell_link_list_device(self, grid, x, h, items, cell_start, cell_of, prec, offsets,
                               items_out):
+        self._bind(offsets)
         check(lib().sphx_cell_link_list_device(self.h, C.byref(grid), x[0].numel(), _dptr3(x),
                                                float(h), items.data_ptr(), cell_start.data_ptr(),
                                                cell_of.data_ptr(), prec, offsets.data_ptr(),
                                                items_out.data_ptr(), items_out.numel()))
 
     def build_rel_coords_device(self, grid, x, rel, cell, cell_of, cell_start, items):
+        self._bind(items)
         check(lib().sphx_build_rel_coords_device(self.h, C.byref(grid), x[0].numel(), _dptr3(x),
                                                  _dptr3(rel), _dptr3(cell), cell_of.data_ptr(),
                                                  cell_start.data_ptr(), items.data_ptr()))
@@ -322,6 +338,7 @@ class Context:
     # ---- slab decomposition (multigpu.py) -----------------------------------------------
     def build_rel_coords_window_device(self, global_grid, local_grid, axis, layer0, x, rel, cell,
                                        cell_of, cell_start, items):
+        self._bind(items)
         check(lib().sphx_build_rel_coords_window_device(
             self.h, C.byref(global_grid), C.byref(local_grid), axis, layer0, x[0].numel(),
             _dptr3(x), _dptr3(rel), _dptr3(cell), cell_of.data_ptr(), cell_start.data_ptr(),
@@ -329,11 +346,13 @@ class Context:
 
     def rcll_rows_device(self, grid, rel, cell, items, cell_start, prec, ids, row0, nrows,
                          offsets, items_out):
+        self._bind(offsets)
         check(lib().sphx_rcll_rows_device(
             self.h, C.byref(grid), rel[0].numel(), _dptr3(rel), _dptr3(cell), items.data_ptr(),
             cell_start.data_ptr(), prec, ids.data_ptr() if ids is not None else None, row0, nrows,
             offsets.data_ptr(), items_out.data_ptr(), items_out.numel()))
 
     def lattice_device(self, dim, lo, hi, ds, id0, x):
+        self._bind(x[0])
         check(lib().sphx_lattice_device(self.h, dim, _d3(lo), _d3(hi), float(ds), id0,
                                         x[0].numel(), _dptr3(x)))

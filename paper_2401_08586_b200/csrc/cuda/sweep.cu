@@ -855,7 +855,8 @@ __global__ void k_encode_runs(int64_t C, int nx, int wrapx, const int32_t* __res
 // each of the three runs that contain cell c (runs centred at cx+1, cx, cx-1,
 // where c is list 0, 1, 2). The record's place in a run is its index in c plus
 // the number of smaller ids in the run's two other cells (cells hold ascending
-// ids), i.e. the position in the id-merge of the three cells.
+// ids), i.e. the position in the id-merge of the three cells. With slab ids the
+// merge key is the output id (each cell is one id-ascending class there).
 template <int D, int P, int MODE>
 __global__ void k_encode_members(int n, int nx, int wrapx, PrecConsts pc,
                                  const int32_t* __restrict__ start,
@@ -889,7 +890,12 @@ __global__ void k_encode_members(int n, int nx, int wrapx, PrecConsts pc,
         continue;
       }
       int cnt = 0;
-      for (int q = lo; q < hi; ++q) cnt += __ldg(items + q) < j;
+      if (a.ids) {  // slab: merge by output (global) id -- in 1-D a run can mix
+        const int gj = __ldg(a.ids + j);  // owned and halo cells
+        for (int q = lo; q < hi; ++q) cnt += __ldg(a.ids + __ldg(items + q)) < gj;
+      } else {
+        for (int q = lo; q < hi; ++q) cnt += __ldg(items + q) < j;
+      }
       pos += cnt;
     }
     const int64_t r = run_record_slot(st, tx, nx, wrapx, (c - cx) + tx) + pos;

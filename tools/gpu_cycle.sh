@@ -2,7 +2,7 @@
 # One GPU iteration (run under gpurun): parity tests, bench, profile.
 #   tools/gpu_cycle.sh <tag> [--no-profile]
 TAG=$1
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_${TAG}.log 2>&1; tail -4 gpurun_out/pytest_${TAG}.log
 python bench.py --no-cpu-baseline > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
 python - "$TAG" <<'PY'
 import json, sys
