@@ -343,6 +343,13 @@ def bench(args, workloads, metric, clock_sampler=None, peaks=(6650.0, "fallback"
     world, rank, local = _env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if "RANK" not in os.environ:  # `bench.py --slab` without torchrun: a world of one
+        import socket
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
+                          MASTER_PORT=str(port))
     dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
