@@ -21,13 +21,11 @@ int launch_encode(int dim, int prec, int mode, int n, int64_t C, int nx, int wra
                   const PrecConsts& pc, const double* const x[3], const int32_t* items,
                   const int32_t* start, void* pos_csr, int32_t* cell_slot, const SweepArgs& a,
                   cudaStream_t st);
-void launch_count(int dim, int prec, int mode, const SweepArgs& a, cudaStream_t st);
-void launch_fill(int dim, int prec, int mode, const SweepArgs& a, cudaStream_t st);
+void launch_sweep(int dim, int prec, int mode, const SweepArgs& a, cudaStream_t st);
 size_t coord_bytes(int dim, int prec);
-size_t quad_bytes(int prec);
+size_t chunk_bytes(int dim, int prec, int mode);
 int64_t chunk_capacity(int mode, int64_t n, int64_t C);
-int fill_tile(int dim);
-int mask_words(int dim);
+int sweep_tile(int dim);
 // binning.cu
 int64_t scan_tiles(int64_t C);
 void launch_locate(int mode, const LocateArgs& a, cudaStream_t st);
@@ -118,7 +116,12 @@ struct sphx_context {
   // inputs staged from host
   Buf in_x[3], in_cell[3], in_items, in_start, in_cellof;
   // encode / sweep scratch
-  Buf pos_own, pos_csr, cell_slot, tri, qx[3], qdc, qtag, rank, selfpos, counts, block_sum, masks;
+  Buf pos_own, pos_csr, cell_slot, tri, qc, qtag, selfpos;
+  // single-pass sweep: look-back words (epoch-tagged) and the tile ticket
+  Buf sw_tiles, sw_ticket;
+  unsigned long long sw_tick = 0;
+  unsigned sw_epoch = 0;
+  int64_t sw_ntiles = 0;
   // table of the last host-API call
   Buf t_offsets, t_items;
   int64_t t_n = -1, t_total = 0, t_capacity = 0;
@@ -273,9 +276,8 @@ int upload(sphx_context* ctx, Buf& b, const void* src, size_t bytes) {
   return SPHX_OK;
 }
 
-// Encode + count + block-sum scan on device pointers (src = rel for RCLL,
-// positions for CLL/ALL). Leaves the exact total in d_off[n] and the sweep
-// arguments in *out for the fill pass.
+// Encode on device pointers (src = rel for RCLL, positions for CLL/ALL): the
+// candidate runs and own-particle data the sweep reads; fills *out for it.
 // Rows to produce: particles [row0, row0 + nrows); ids = output id of each
 // particle (null: its index). The multi-GPU slab path asks for the owned rows
 // of a slab-local system with global ids.
@@ -300,45 +302,33 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
   out->row0 = (int)sel.row0;
   out->nrows = (int)nrows;
   out->ids = sel.ids;
+  out->offsets = d_off;
   if (n == 0 || nrows == 0) {
     CK(cudaMemsetAsync(d_off, 0, sizeof(int64_t), st));
     return SPHX_OK;
   }
   const int64_t C = mode == MODE_ALL ? 0 : cell_total(g);
   const int64_t chunks = chunk_capacity(mode, n, C);
-  const int nb = (int)((nrows + fill_tile(g.dim) - 1) / fill_tile(g.dim));
   TRY(ctx->pos_own.ensure(coord_bytes(g.dim, prec) * (size_t)n));
-  for (int k = 0; k < g.dim; ++k) TRY(ctx->qx[k].ensure(quad_bytes(prec) * (size_t)chunks));
+  TRY(ctx->qc.ensure(chunk_bytes(g.dim, prec, mode) * (size_t)chunks));
   TRY(ctx->qtag.ensure(16 * (size_t)chunks));
-  if (mode == MODE_RCLL) TRY(ctx->qdc.ensure(quad_bytes(prec) * (size_t)chunks));
   if (mode != MODE_ALL) {
     TRY(ctx->pos_csr.ensure(coord_bytes(g.dim, prec) * (size_t)n));
     TRY(ctx->cell_slot.ensure(sizeof(int32_t) * (size_t)n));
     TRY(ctx->tri.ensure(sizeof(int2) * std::max<int64_t>(C, 1)));
-    TRY(ctx->rank.ensure(sizeof(int32_t) * (size_t)n));
     TRY(ctx->selfpos.ensure(sizeof(int32_t) * (size_t)n));
   }
-  TRY(ctx->masks.ensure(sizeof(unsigned) * mask_words(g.dim) * (size_t)n));
-  TRY(ctx->counts.ensure(sizeof(int32_t) * n));
-  TRY(ctx->block_sum.ensure(sizeof(long long) * nb));
 
   SweepArgs& a = *out;
   a.g = grid_consts(g);
   a.c = make_consts(mode, prec, g, h);
   a.tri = ctx->tri.as<int2>();
-  for (int k = 0; k < 3; ++k) a.qx[k] = ctx->qx[k].p;
-  a.qdc = ctx->qdc.p;
+  a.qc = ctx->qc.p;
   a.qtag = ctx->qtag.p;
   a.selfpos = ctx->selfpos.as<int32_t>();
-  a.rank = ctx->rank.as<int32_t>();
-  a.order = mode == MODE_ALL ? nullptr : items;
   a.pos_own = ctx->pos_own.p;
   for (int k = 0; k < 3; ++k) a.cellk[k] = cellk ? cellk[k] : nullptr;
   a.cell_of = cell_of;
-  a.offsets = d_off;
-  a.counts = ctx->counts.as<int32_t>();
-  a.masks = ctx->masks.as<unsigned>();
-  a.block_sum = ctx->block_sum.as<long long>();
 
   if (ctx->timing) CK(cudaEventRecord(ctx->ev[0], st));
   ctx->launches += launch_encode(g.dim, prec, mode, n, C, a.g.counts[0], a.g.wrap[0], a.c, src,
@@ -346,36 +336,55 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
                                  st);
   CKL();
   if (ctx->timing) CK(cudaEventRecord(ctx->ev[1], st));
-  launch_count(g.dim, prec, mode, a, st);
-  CKL();
-  ctx->launches += 3;
   return SPHX_OK;
 }
 
-int run_fill(sphx_context* ctx, int mode, int dim, int prec, SweepArgs& a, int32_t* d_items,
-             int64_t capacity) {
+// The single-pass sweep: offsets (always) and the rows (where they fit in
+// `capacity`; the exact total is d_off[nrows] either way).
+int run_sweep(sphx_context* ctx, int dim, int prec, int mode, SweepArgs& a, int32_t* d_items,
+              int64_t capacity) {
   if (a.n == 0 || a.nrows == 0) return SPHX_OK;
+  cudaStream_t st = ctx->stream;
+  const int64_t nt = (a.nrows + sweep_tile(dim) - 1) / sweep_tile(dim);
+  if (nt > ctx->sw_ntiles || ctx->sw_epoch >= 0xFFFFu) {
+    // fresh (or recycled) look-back words: epoch 0 marks them unpublished
+    TRY(ctx->sw_tiles.ensure(sizeof(unsigned long long) * std::max<int64_t>(nt, ctx->sw_ntiles)));
+    ctx->sw_ntiles = std::max<int64_t>(nt, ctx->sw_ntiles);
+    CK(cudaMemsetAsync(ctx->sw_tiles.p, 0, sizeof(unsigned long long) * ctx->sw_ntiles, st));
+    ctx->sw_epoch = 0;
+  }
+  if (!ctx->sw_ticket.p) {
+    TRY(ctx->sw_ticket.ensure(sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(ctx->sw_ticket.p, 0, sizeof(unsigned long long), st));
+    ctx->sw_tick = 0;
+  }
   a.items = d_items;
   a.capacity = capacity;
-  launch_fill(dim, prec, mode, a, ctx->stream);
+  a.tiles = ctx->sw_tiles.as<unsigned long long>();
+  a.ticket = ctx->sw_ticket.as<unsigned long long>();
+  a.tick0 = ctx->sw_tick;
+  a.epoch = ++ctx->sw_epoch;
+  launch_sweep(dim, prec, mode, a, st);
   CKL();
+  ctx->sw_tick += (unsigned long long)nt;
   ++ctx->launches;
-  if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], ctx->stream));
+  if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], st));
   return SPHX_OK;
 }
 
-// Device API: all passes, no synchronisation (capacity overflow is detectable by
-// the caller through d_off[n]).
+// Device API: encode + sweep, no synchronisation (capacity overflow is
+// detectable by the caller through d_off[n]).
 int run_nnps(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n,
              const double* const src[3], const int32_t* const cellk[3], const int32_t* items,
              const int32_t* start, const int32_t* cell_of, int prec, double h, int64_t* d_off,
              int32_t* d_items, int64_t capacity) {
   SweepArgs a;
   TRY(run_prepare(ctx, mode, g, n, src, cellk, items, start, cell_of, prec, h, d_off, &a));
-  return run_fill(ctx, mode, g.dim, prec, a, d_items, capacity);
+  return run_sweep(ctx, g.dim, prec, mode, a, d_items, capacity);
 }
 
-// Host-API driver: count, read the exact total, size the table, fill.
+// Host-API driver: encode, sweep into the context's table, read the exact total;
+// if the table was too small, grow it and sweep again (the encode is reused).
 int run_host_table(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n,
                    const double* const d_src[3], const int32_t* const d_cellk[3],
                    const int32_t* d_items, const int32_t* d_start, const int32_t* d_cellof,
@@ -384,15 +393,23 @@ int run_host_table(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t
   SweepArgs a;
   TRY(run_prepare(ctx, mode, g, n, d_src, d_cellk, d_items, d_start, d_cellof, prec, h,
                   ctx->t_offsets.as<int64_t>(), &a));
+  if (ctx->t_capacity == 0) {
+    // first table on this context: room for the typical row lengths of a
+    // uniform distribution at kh = 2.4 ds (2-D ~18, 3-D ~57)
+    const int64_t per = g.dim == 3 ? 64 : (g.dim == 2 ? 24 : 6);
+    ctx->t_capacity = std::max<int64_t>(per * n, 1024);
+    TRY(ctx->t_items.ensure(sizeof(int32_t) * ctx->t_capacity));
+  }
   int64_t tot = 0;
-  CK(cudaMemcpyAsync(&tot, ctx->t_offsets.as<int64_t>() + n, sizeof(int64_t),
-                     cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  if (tot > ctx->t_capacity) {
+  for (int pass = 0; pass < 2; ++pass) {
+    TRY(run_sweep(ctx, g.dim, prec, mode, a, ctx->t_items.as<int32_t>(), ctx->t_capacity));
+    CK(cudaMemcpyAsync(&tot, ctx->t_offsets.as<int64_t>() + n, sizeof(int64_t),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (tot <= ctx->t_capacity) break;
     ctx->t_capacity = tot + tot / 16 + 1024;
     TRY(ctx->t_items.ensure(sizeof(int32_t) * ctx->t_capacity));
   }
-  TRY(run_fill(ctx, mode, g.dim, prec, a, ctx->t_items.as<int32_t>(), ctx->t_capacity));
   ctx->t_n = n;
   ctx->t_total = tot;
   *total = tot;
@@ -530,8 +547,8 @@ void sphx_destroy(sphx_context* ctx) {
   cudaStreamSynchronize(ctx->stream);
   Buf* all[] = {&ctx->in_x[0], &ctx->in_x[1], &ctx->in_x[2], &ctx->in_cell[0], &ctx->in_cell[1],
                 &ctx->in_cell[2], &ctx->in_items, &ctx->in_start, &ctx->in_cellof, &ctx->pos_own,
-                &ctx->tri, &ctx->pos_csr, &ctx->cell_slot, &ctx->qx[0], &ctx->qx[1], &ctx->qx[2], &ctx->qdc,
-                &ctx->qtag, &ctx->rank, &ctx->selfpos, &ctx->counts, &ctx->block_sum, &ctx->masks, &ctx->t_offsets, &ctx->t_items,
+                &ctx->tri, &ctx->pos_csr, &ctx->cell_slot, &ctx->qc,
+                &ctx->qtag, &ctx->selfpos, &ctx->sw_tiles, &ctx->sw_ticket, &ctx->t_offsets, &ctx->t_items,
                 &ctx->b_counts, &ctx->b_slot, &ctx->b_bad, &ctx->b_tiles, &ctx->b_out_cellof,
                 &ctx->b_out_start, &ctx->b_out_items, &ctx->b_rel[0], &ctx->b_rel[1],
                 &ctx->b_rel[2], &ctx->b_cell[0], &ctx->b_cell[1], &ctx->b_cell[2]};
@@ -790,7 +807,7 @@ int sphx_rcll_rows_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t
   SweepArgs a;
   TRY(run_prepare(ctx, MODE_RCLL, *grid, n, d_rel, d_cell, d_items, d_cell_start, nullptr,
                   precision, 0.0, d_offsets, &a, sel));
-  return run_fill(ctx, MODE_RCLL, grid->dim, precision, a, d_items_out, capacity);
+  return run_sweep(ctx, grid->dim, precision, MODE_RCLL, a, d_items_out, capacity);
 }
 
 int sphx_build_rel_coords_window_device(sphx_context* ctx, const sphx_grid_desc* global,

@@ -31,30 +31,29 @@ struct GridConsts {
   int wrap[3];  // periodic(k) && count(k) > 2  (nnps.cpp:223, :364)
 };
 
-// Arguments of the sweep kernels (encode writes the candidate arrays, count and
-// fill read them).
+// Arguments of the sweep kernels (encode writes the candidate arrays, the
+// single-pass sweep reads them).
 struct SweepArgs {
   int n;
   GridConsts g;
   PrecConsts c;
   int2* tri;                  // [C] chunk run [x, y) of each cell's x-triple
-  void* qx[3];                // [chunks] coordinate quads per axis (x pre-shifted for CLL)
-  void* qdc;                  // [chunks] RCLL x offset quads dc = cx_i - cx_j
+  void* qc;                   // [chunks] records: coordinate quads per axis (x pre-shifted
+                              // for CLL), then the RCLL x offset quad dc = cx_i - cx_j
   void* qtag;                 // [chunks] uint4 particle ids (~0 = sentinel)
   int32_t* selfpos;           // [n] record index of particle i in its own-cell run
-  int32_t* rank;              // [n] CSR slot of particle i (masks are slot-indexed)
-  const int32_t* order;       // CSR slot -> particle (CellGrid::items), null = identity
   const void* pos_own;        // packed coords in particle order
   const int32_t* cellk[3];    // RCLL: RelCoords::cell[k] (particle order)
   const int32_t* cell_of;     // CLL:  CellGrid::cell_of  (particle order)
-  int64_t* offsets;           // [n+1]
+  int64_t* offsets;           // [nrows+1]
   int32_t* items;             // [capacity]
   int64_t capacity;
   int row0, nrows;            // rows produced: particles [row0, row0 + nrows)
   const int32_t* ids;         // output id of particle j (null: j) -- global ids of a slab
-  int32_t* counts;            // [n] row lengths (pass 1), bit 31: masks overflowed
-  unsigned* masks;            // [W][n] hit nibbles of every 4-record chunk (pass 1)
-  long long* block_sum;       // [blocks] row-length sums, scanned in place (pass 2)
+  unsigned long long* tiles;  // [tiles] look-back words (epoch-tagged, never cleared)
+  unsigned long long* ticket; // tile ticket counter (monotone across calls)
+  unsigned long long tick0;   // ticket value at this call's first tile
+  unsigned epoch;             // this call's look-back epoch (1..65535)
 };
 
 // Look-back words carry flag and value in one 64-bit word, so relaxed gpu-scope

@@ -18,11 +18,11 @@
 // periodic x shift already applied (round_to(prec, xj + shift), nnps.cpp:116).
 // A particle's candidates are the 3 (2-D) / 9 (3-D) runs of its (dy, dz) rows.
 //
-// Passes:  count (distance tests, one per candidate; hit nibbles + row lengths)
-//          -> tile sums -> scan -> fill (hit ids from the nibbles into sorted,
-//          warp-packed rows in shared memory, coalesced stores to HBM).
-// Count runs in cell (CSR) order so the lanes of one cell share every record;
-// fill runs in particle order so the 32 rows of a warp are one contiguous run.
+// One pass (k_sweep) over tiles of consecutive rows (particle order): distance
+// tests of every candidate, sorted rows in shared memory, a block scan plus a
+// decoupled look-back for the row offsets, and 16-byte stores of the packed
+// tile. Consecutive particles share cells in lattice and cell-sorted orders, so
+// a tile's candidate loads are L1 hits; in any order they are L2 hits.
 //
 // Bit-exactness: every step is an explicit round-to-nearest op in the
 // precision (no contraction; the reference is built without -march). The x term
@@ -198,10 +198,44 @@ struct Chunk {
   typename Prec<P>::Quad dc;
 };
 
+// Chunks are stored array-of-structures: one record of NQ quads (the D
+// coordinate quads, then the RCLL dc quad), padded to a power of two, so a
+// chunk is one 32-byte sector at FP16 and is fetched with 16-byte loads.
+template <int D, int P, int MODE>
+struct ChunkLay {
+  static constexpr int QB = P == FP16 ? 8 : (P == FP32 ? 16 : 32);  // bytes per quad
+  static constexpr int NQ = D + (MODE == MODE_RCLL ? 1 : 0);
+  static constexpr int NQP = NQ <= 1 ? 1 : (NQ <= 2 ? 2 : 4);
+  static constexpr int BYTES = QB * NQP;
+};
+
+// element u (0..3) of quad q of chunk ch
+template <int D, int P, int MODE>
+__device__ __forceinline__ typename Prec<P>::T* rec_el(void* qc, int64_t ch, int q, int u) {
+  using L = ChunkLay<D, P, MODE>;
+  return reinterpret_cast<typename Prec<P>::T*>(static_cast<char*>(qc) + ch * L::BYTES +
+                                                q * L::QB) + u;
+}
+
 // 4 lane masks of a pair of HSET2 results -> 4-bit hit nibble (record order)
 __device__ __forceinline__ unsigned nibble(unsigned mk01, unsigned mk23) {
   const unsigned w = __byte_perm(mk01, mk23, 0x6420) & 0x08040201u;
   return (w * 0x01010101u) >> 24;
+}
+
+// acc = acc >> 4 | nibble << 28, the nibble being the 4 tests acc_u < thr of two
+// binary16x2 accumulators (records 0,1 in a01, 2,3 in a23); NaN never hits.
+__device__ __forceinline__ void acc_nibble(unsigned& acc, __half2 a01, __half2 a23, __half2 thr2) {
+  asm("{\n\t.reg .pred p0, p1, p2, p3;\n\t"
+      "setp.lt.f16x2 p0|p1, %1, %3;\n\t"
+      "setp.lt.f16x2 p2|p3, %2, %3;\n\t"
+      "shr.b32 %0, %0, 4;\n\t"
+      "@p0 or.b32 %0, %0, 0x10000000;\n\t"
+      "@p1 or.b32 %0, %0, 0x20000000;\n\t"
+      "@p2 or.b32 %0, %0, 0x40000000;\n\t"
+      "@p3 or.b32 %0, %0, 0x80000000;\n\t}"
+      : "+r"(acc)
+      : "r"(h2u(a01)), "r"(h2u(a23)), "r"(h2u(thr2)));
 }
 
 // row constant: +-v for a -1/+1 row offset (as dc = -off), +0 for the centre row
@@ -260,6 +294,9 @@ struct Tester<D, FP16, MODE_RCLL> {
   __device__ __forceinline__ unsigned test4(const Row& r, const Chunk<D, FP16>& ch) const {
     return nibble(__hlt2_mask(pair_acc(r, ch, false), thr2), __hlt2_mask(pair_acc(r, ch, true), thr2));
   }
+  __device__ __forceinline__ void acc4(const Row& r, const Chunk<D, FP16>& ch, unsigned& acc) const {
+    acc_nibble(acc, pair_acc(r, ch, false), pair_acc(r, ch, true), thr2);
+  }
 };
 
 // ---- CLL / all_list, FP16 (dist_prec nnps.cpp:112-121; nnps_batch.cpp:145-157) ----
@@ -299,6 +336,9 @@ struct TesterHalfAbs {
   }
   __device__ __forceinline__ unsigned test4(const Row& r, const Chunk<D, FP16>& ch) const {
     return nibble(__hlt2_mask(pair_acc(r, ch, false), thr2), __hlt2_mask(pair_acc(r, ch, true), thr2));
+  }
+  __device__ __forceinline__ void acc4(const Row& r, const Chunk<D, FP16>& ch, unsigned& acc) const {
+    acc_nibble(acc, pair_acc(r, ch, false), pair_acc(r, ch, true), thr2);
   }
 };
 template <int D> struct Tester<D, FP16, MODE_CLL> : TesterHalfAbs<D, MODE_CLL> {};
@@ -346,6 +386,9 @@ struct TesterRcllScalar {
     }
     return m;
   }
+  __device__ __forceinline__ void acc4(const Row& r, const Chunk<D, P>& ch, unsigned& acc) const {
+    acc = (acc >> 4) | (test4(r, ch) << 28);
+  }
 };
 
 // ---- CLL / all_list, FP32 / FP64 (dist_prec nnps.cpp:94-111) ----
@@ -391,6 +434,9 @@ struct TesterAbsScalar {
     }
     return m;
   }
+  __device__ __forceinline__ void acc4(const Row& r, const Chunk<D, P>& ch, unsigned& acc) const {
+    acc = (acc >> 4) | (test4(r, ch) << 28);
+  }
 };
 
 template <int D> struct Tester<D, FP32, MODE_RCLL> : TesterRcllScalar<D, FP32> {};
@@ -402,10 +448,23 @@ template <int D> struct Tester<D, FP64, MODE_ALL> : TesterAbsScalar<D, FP64> {};
 
 template <int D, int P, int MODE>
 __device__ __forceinline__ void load_chunk(const SweepArgs& a, int64_t ch, Chunk<D, P>& c) {
+  using L = ChunkLay<D, P, MODE>;
   using Q = typename Prec<P>::Quad;
+  if constexpr (L::BYTES >= 16) {
+    constexpr int NV = L::BYTES / 16;
+    union {
+      uint4 v[NV];
+      Q q[L::NQP];
+    } u;
+    const uint4* p = reinterpret_cast<const uint4*>(static_cast<const char*>(a.qc) + ch * L::BYTES);
 #pragma unroll
-  for (int k = 0; k < D; ++k) c.x[k] = ldg<Q>(a.qx[k], ch);
-  if constexpr (MODE == MODE_RCLL) c.dc = ldg<Q>(a.qdc, ch);
+    for (int v = 0; v < NV; ++v) u.v[v] = __ldg(p + v);
+#pragma unroll
+    for (int k = 0; k < D; ++k) c.x[k] = u.q[k];
+    if constexpr (MODE == MODE_RCLL) c.dc = u.q[D];
+  } else {  // FP16 1-D CLL/all: one 8-byte quad
+    c.x[0] = __ldg(reinterpret_cast<const Q*>(a.qc) + ch);
+  }
 }
 
 // ------------------------------------------------------------------------------
@@ -470,282 +529,454 @@ __device__ __forceinline__ void visit_rows(const SweepArgs& a, int i, Fn&& fn) {
   }
 }
 
-// Distance tests of particle i against every candidate chunk. fn(m, ch) gets the
-// hit nibble of chunk ch (bit u: record 4ch+u is a neighbour j != i). The own
-// record (id i) sits in the own-cell run at selfpos[i] and is masked out there.
-template <int D, int P, int MODE, class ChunkFn>
-__device__ __forceinline__ void scan_particle(const SweepArgs& a, int i, ChunkFn&& fn) {
-  using Tst = Tester<D, P, MODE>;
-  Tst tst;
-  tst.init(a, i);
-  const int64_t self = MODE == MODE_ALL ? (int64_t)i : (int64_t)__ldg(a.selfpos + i);
-  visit_rows<D, MODE>(a, i, [&](int dy, int dz, int wy, int wz, int cb, int ce) {
-    const typename Tst::Row row = tst.row(a, dy, dz, wy, wz);
-    const bool own = dy == 0 && dz == 0;
-#pragma unroll 4
-    for (int ch = cb; ch < ce; ++ch) {
-      Chunk<D, P> c;
-      load_chunk<D, P, MODE>(a, ch, c);
-      unsigned m = tst.test4(row, c);
-      if (own) {
-        const int64_t d = self - 4 * (int64_t)ch;
-        if (d >= 0 && d < 4) m &= ~(1u << d);
-      }
-      if (MODE == MODE_ALL) {  // the single run ends exactly at n
-        const int64_t left = a.n - 4 * (int64_t)ch;
-        if (left < 4) m &= (1u << left) - 1u;
-      }
-      fn(m, ch);
-    }
-  });
-}
-
-template <int D>
-struct MaskWords {  // 32-bit words of 4-bit hit nibbles per particle
-  static constexpr int W = D == 3 ? 16 : (D == 2 ? 4 : 2);
-};
-constexpr unsigned kOverflow = 0x80000000u;  // counts[i] flag: nibbles did not fit
-
-// Pass 1 (cell order): row lengths k_i and the hit nibbles of every chunk.
-template <int D, int P, int MODE, int BT>
-__global__ void __launch_bounds__(BT) k_count(SweepArgs a) {
-  constexpr int W = MaskWords<D>::W;
-  const int s = blockIdx.x * BT + threadIdx.x;
-  if (s >= a.n) return;
-  const int i = a.order ? __ldg(a.order + s) : s;
-  if (i < a.row0 || i >= a.row0 + a.nrows) return;  // not a requested row (or malformed)
-  int k = 0, bits = 0, words = 0;
+// Hit words. The chunks of each run are tested in groups of up to 8; the 4-bit
+// hit nibbles of a group form one 32-bit word, chunk g at bits 0-3 (bit u of a
+// nibble: record u is a neighbour j != i). The own record (particle i) sits in
+// its own-cell run at selfpos[i] and is masked out there.
+template <int D, int P, int MODE>
+__device__ __forceinline__ unsigned group_word(const SweepArgs& a, const Tester<D, P, MODE>& tst,
+                                               const typename Tester<D, P, MODE>::Row& row,
+                                               bool own, int selfch, unsigned selfmask, int g,
+                                               int e) {
   unsigned acc = 0;
-  scan_particle<D, P, MODE>(a, i, [&](unsigned m, int64_t) {
-    k += __popc(m);
-    acc |= m << bits;
-    bits += 4;
-    if (bits == 32) {
-      if (words < W) a.masks[(int64_t)words * a.n + s] = acc;
-      ++words;
-      acc = 0;
-      bits = 0;
-    }
+#pragma unroll 4
+  for (int ch = g; ch < e; ++ch) {
+    Chunk<D, P> c;
+    load_chunk<D, P, MODE>(a, ch, c);
+    tst.acc4(row, c, acc);
+    if (own && ch == selfch) acc &= selfmask;
+  }
+  return acc >> (4 * (8 - (e - g)));
+}
+
+// Calls fn(row, own, g, e) for every group [g, e) of chunks of particle i, in
+// row order ((dz, dy) ascending; runs are id-merged, so hits come out sorted
+// inside each run).
+template <int D, int P, int MODE, class Fn>
+__device__ __forceinline__ void walk_groups(const SweepArgs& a, int i, const Tester<D, P, MODE>& tst,
+                                            Fn&& fn) {
+  visit_rows<D, MODE>(a, i, [&](int dy, int dz, int wy, int wz, int cb, int ce) {
+    const typename Tester<D, P, MODE>::Row row = tst.row(a, dy, dz, wy, wz);
+    const bool own = dy == 0 && dz == 0;
+    for (int g = cb; g < ce; g += 8) fn(row, own, g, min(g + 8, ce));
   });
-  if (bits) {
-    if (words < W) a.masks[(int64_t)words * a.n + s] = acc;
-    ++words;
-  }
-  a.counts[i] = (int)((unsigned)k | (words > W ? kOverflow : 0u));
 }
 
-// Pass 2a: row-length sums of tiles of `tile` consecutive particles.
-__global__ void __launch_bounds__(256) k_tile_sums(const int32_t* __restrict__ counts, int n, int tile,
-                                                   long long* __restrict__ sums) {
-  __shared__ long long s_w[8];
-  const int64_t base = (int64_t)blockIdx.x * tile;
-  long long v = 0;
-  for (int q = threadIdx.x; q < tile; q += 256) {
-    const int64_t i = base + q;
-    if (i < n) v += (int)((unsigned)__ldg(counts + i) & ~kOverflow);
+// Row sinks: a row being built in shared memory (32-bit shared address, so each
+// store is one STS) or straight in HBM (tiles whose rows exceed the tile buffer).
+struct SharedRow {
+  uint32_t base;  // shared-space byte address of element 0
+  __device__ __forceinline__ void st(int e, int v) const {
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(base + 4u * (uint32_t)e), "r"(v) : "memory");
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    long long t = 0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) t += s_w[w];
-    sums[blockIdx.x] = t;
+  __device__ __forceinline__ int ld(int e) const {
+    int v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(base + 4u * (uint32_t)e) : "memory");
+    return v;
   }
-}
+};
+struct GlobalRow {
+  int32_t* p;
+  __device__ __forceinline__ void st(int e, int v) const { p[e] = v; }
+  __device__ __forceinline__ int ld(int e) const { return p[e]; }
+};
 
-// Pass 2b: exclusive scan of the tile sums in place (one block); offsets[n] = total.
-__global__ void __launch_bounds__(1024) k_scan_blocks(long long* sums, int nb, int64_t* offsets,
-                                                      int n) {
-  __shared__ long long s_w[32];
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int per = (nb + 1023) / 1024;
-  const int b0 = t * per, b1 = min(b0 + per, nb);
-  long long local = 0;
-  for (int b = b0; b < b1; ++b) local += sums[b];
-  long long incl = local;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const long long u = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += u;
-  }
-  if (lane == 31) s_w[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    const long long w = s_w[lane];
-    long long wi = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const long long u = __shfl_up_sync(0xffffffffu, wi, o);
-      if (lane >= o) wi += u;
-    }
-    s_w[lane] = wi - w;
-    if (lane == 31) offsets[n] = wi;
-  }
-  __syncthreads();
-  long long run = s_w[warp] + incl - local;
-  for (int b = b0; b < b1; ++b) {
-    const long long s = sums[b];
-    sums[b] = run;
-    run += s;
-  }
-}
-
-// ------------------------------------------------------------------------------
-// Row assembly (pass 3)
-// ------------------------------------------------------------------------------
-// Sorted insertion of a chunk's hits (ids ascending within the chunk, since runs
-// are id-sorted). Fast path: the chunk's first hit is >= the row's last id, so
-// the hits are appended as they are.
+// Appends the hits of one chunk (nibble m, ids tq) to dst[k..]: predicated
+// stores at the prefix positions, no branches.
 template <class Row>
-__device__ __forceinline__ void emit4(Row& row, int& k, int& last, unsigned m, const uint4& tq) {
-  const int j[4] = {(int)tq.x, (int)tq.y, (int)tq.z, (int)tq.w};
-  const int first = (m & 1u) ? j[0] : ((m & 2u) ? j[1] : ((m & 4u) ? j[2] : j[3]));
-  if (first >= last) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (m >> u & 1u) {
-        row[k] = j[u];
-        ++k;
-        last = j[u];
-      }
-    }
-  } else {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (m >> u & 1u) {
-        const int v = j[u];
-        int q = k;
-        int w;
-        while (q > 0 && (w = row[q - 1]) > v) {
-          row[q] = w;
-          --q;
-        }
-        row[q] = v;
-        ++k;
-        last = max(last, v);
-      }
+__device__ __forceinline__ void append4(const Row& dst, int& k, unsigned m, const uint4& tq) {
+  const int p1 = k + (int)(m & 1u);
+  const int p2 = p1 + (int)((m >> 1) & 1u);
+  const int p3 = p2 + (int)((m >> 2) & 1u);
+  if (m & 1u) dst.st(k, (int)tq.x);
+  if (m & 2u) dst.st(p1, (int)tq.y);
+  if (m & 4u) dst.st(p2, (int)tq.z);
+  if (m & 8u) dst.st(p3, (int)tq.w);
+  k = p3 + (int)(m >> 3);
+}
+
+// dst[0, gs) and dst[gs, k) are each sorted: insert the tail into the head. Once
+// a tail element is already above everything before it, the rest are too.
+template <class Row>
+__device__ __forceinline__ void merge_tail(const Row& dst, int gs, int k) {
+  for (int e = gs; e < k; ++e) {
+    const int v = dst.ld(e);
+    int w = dst.ld(e - 1);
+    if (w < v) break;
+    int q = e;
+    do {
+      dst.st(q, w);
+      --q;
+    } while (q > 0 && (w = dst.ld(q - 1)) > v);
+    dst.st(q, v);
+  }
+}
+
+// Streams the packed tile pk[0, n) to gout: 16-byte stores on the aligned
+// vectors of gout, element stores at the two ragged ends.
+template <int BT>
+__device__ __forceinline__ void stream_tile(int32_t* gout, const SharedRow& pk, int n, int tid) {
+  const int ph = (int)(((uintptr_t)gout & 15u) >> 2);
+  int4* g4 = reinterpret_cast<int4*>(gout - ph);
+  const int nv = (ph + n + 3) >> 2;
+  for (int q = tid; q < nv; q += BT) {
+    const int e0 = 4 * q - ph;  // tile index of the vector's first element
+    if (e0 >= 0 && e0 + 4 <= n) {
+      g4[q] = make_int4(pk.ld(e0), pk.ld(e0 + 1), pk.ld(e0 + 2), pk.ld(e0 + 3));
+    } else {
+      for (int e = max(e0, 0); e < min(e0 + 4, n); ++e) gout[e] = pk.ld(e);
     }
   }
 }
 
-// Replays particle i's hits into row[0..k): from its nibbles (masks at slot s),
-// or by re-testing when they did not fit.
-template <int D, int P, int MODE, class Row>
-__device__ __forceinline__ void build_row(const SweepArgs& a, int i, int64_t s, bool retest,
-                                          Row& row) {
-  int k = 0, last = INT_MIN;
-  const uint4* qtag = reinterpret_cast<const uint4*>(a.qtag);
-  if (!retest) {
-    constexpr int W = MaskWords<D>::W;
-    unsigned acc = 0;
-    int bits = 32, words = 0;
-    auto next = [&]() {
-      if (bits == 32) {
-        acc = words < W ? __ldg(a.masks + (int64_t)words * a.n + s) : 0u;
-        ++words;
-        bits = 0;
-      }
-      const unsigned m = (acc >> bits) & 0xFu;
-      bits += 4;
-      return m;
-    };
-    visit_rows<D, MODE>(a, i, [&](int, int, int, int, int cb, int ce) {
-      // groups of 4 chunks: the id quads of all hit chunks are loaded together
-      for (int ch = cb; ch < ce; ch += 4) {
-        unsigned m[4];
-        uint4 tq[4];
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          m[g] = ch + g < ce ? next() : 0u;
-          if (m[g]) tq[g] = __ldg(qtag + ch + g);
-        }
-#pragma unroll
-        for (int g = 0; g < 4; ++g)
-          if (m[g]) emit4(row, k, last, m[g], tq[g]);
-      }
-    });
-  } else {
-    scan_particle<D, P, MODE>(a, i, [&](unsigned m, int64_t ch) {
-      if (m) emit4(row, k, last, m, __ldg(qtag + ch));
-    });
-  }
+// Decoupled look-back over the tiles of one call. Tile words carry the call's
+// epoch, so the array is never cleared between calls:
+//   [63:48] epoch, [47:46] flag (1 = aggregate, 2 = inclusive prefix), [45:0] value.
+// Publishing (one lane) and resolving (one warp) are separate so that a tile can
+// build its rows while its predecessors finish.
+__device__ __forceinline__ void lookback_publish(unsigned long long* tiles, int bid, long long total,
+                                                 unsigned epoch) {
+  const unsigned long long E = (unsigned long long)epoch << 48;
+  st_release_u64(&tiles[bid], E | ((bid == 0 ? 2ull : 1ull) << 46) | (unsigned long long)total);
 }
 
-// Pass 3 (particle order): offsets[i] and the rows. A warp's 32 rows are one
-// contiguous run of the table: they are built directly at their packed places
-// in shared memory and streamed out with coalesced stores. Rows longer than CAP
-// are built straight in global memory.
-template <int D, int P, int MODE, int BT, int CAP>
-__global__ void __launch_bounds__(BT) k_fill(SweepArgs a) {
-  static_assert(BT % 32 == 0, "shape");
-  __shared__ int32_t S[BT * CAP];
+__device__ __forceinline__ long long lookback_resolve(unsigned long long* tiles, int bid,
+                                                      long long total, unsigned epoch) {
+  if (bid == 0) return 0;
+  const unsigned long long E = (unsigned long long)epoch << 48, PRE = 2ull << 46,
+                           VAL = (1ull << 46) - 1;
+  const int lane = threadIdx.x & 31;
+  long long excl = 0;
+  int p = bid - 1;
+  unsigned backoff = 64;
+  while (true) {
+    const int idx = p - lane;
+    const unsigned long long st = idx >= 0 ? ld_acquire_u64(&tiles[idx]) : (E | PRE);
+    const unsigned flag = (st >> 48) == epoch ? (unsigned)(st >> 46) & 3u : 0u;
+    const unsigned pre_mask = __ballot_sync(0xffffffffu, flag == 2u);
+    const unsigned zero_mask = __ballot_sync(0xffffffffu, flag == 0u);
+    const int first = pre_mask ? __ffs(pre_mask) - 1 : 32;
+    const unsigned need = first >= 31 ? 0xffffffffu : ((2u << first) - 1u);
+    if (zero_mask & need) {
+      __nanosleep(backoff);
+      backoff = backoff < 1024 ? backoff * 2 : 1024;
+      continue;
+    }
+    const long long v = lane <= first ? (long long)(st & VAL) : 0ll;
+    excl += warp_sum_ll(v);
+    if (first < 32) break;
+    p -= 32;
+  }
+  if (lane == 0) st_release_u64(&tiles[bid], E | PRE | (unsigned long long)(excl + total));
+  return excl;
+}
+
+// ------------------------------------------------------------------------------
+// FP16 RCLL, 2-D / 3-D: the hot path, written out without the generic walk.
+// Per particle the 3^(d-1) runs (dz, dy ascending) are resolved once into
+// registers; each chunk is one 32-byte record {x quad, y quad, (z quad,) dc quad}.
+// Per pair of candidates and axis: s = r16(ri - rj); t = r16(s * r16(hc/2));
+// d = r16(t + r16(dc*hc)) (x: one fused dc*hc16 + t, dc*hc16 exact) or
+// r16(t + cc_row) (y, z; skipped for the centre row, where cc = 0 and t + 0 == t);
+// acc = r16(acc + r16(d*d)); hit: acc < thr (nnps.cpp:332-346, nnps_batch.cpp:238-258).
+// ------------------------------------------------------------------------------
+template <int D>
+struct R16 {
+  static constexpr int NR = D == 3 ? 9 : 3;  // runs per particle
+  static constexpr int CENTRE = NR / 2;      // dy = dz = 0
+};
+
+template <int D, int R>
+__device__ __forceinline__ unsigned r16_group(const char* __restrict__ qc, int g, int e,
+                                              const __half2 (&r2)[3], const __half2 (&hh2)[3],
+                                              __half2 hc2, __half2 thr2, __half2 ccy, __half2 ccz,
+                                              int selfch, unsigned selfmask) {
+  constexpr int dy = D == 3 ? (R % 3) - 1 : R - 1;
+  constexpr int dz = D == 3 ? (R / 3) - 1 : 0;
+  unsigned acc = 0;
+#pragma unroll 4
+  for (int ch = g; ch < e; ++ch) {
+    const uint4* p = reinterpret_cast<const uint4*>(qc + (size_t)ch * 32);
+    const uint4 v0 = __ldg(p);
+    uint4 v1;
+    if constexpr (D == 3) v1 = __ldg(p + 1);
+    else {
+      const uint2 t = __ldg(reinterpret_cast<const uint2*>(p + 1));
+      v1 = make_uint4(t.x, t.y, 0u, 0u);
+    }
+    // quads: x = (v0.x, v0.y), y = (v0.z, v0.w), 3-D z = (v1.x, v1.y), dc = last quad
+    const unsigned dcl = D == 3 ? v1.z : v1.x, dch = D == 3 ? v1.w : v1.y;
+    __half2 a[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const unsigned xj = h ? v0.y : v0.x, yj = h ? v0.w : v0.z;
+      __half2 t = __hmul2_rn(__hsub2_rn(r2[0], u2h(xj)), hh2[0]);
+      __half2 d = __hfma2(u2h(h ? dch : dcl), hc2, t);
+      __half2 acc2 = __hmul2_rn(d, d);
+      t = __hmul2_rn(__hsub2_rn(r2[1], u2h(yj)), hh2[1]);
+      if constexpr (dy != 0) t = __hadd2_rn(t, ccy);
+      acc2 = __hadd2_rn(acc2, __hmul2_rn(t, t));
+      if constexpr (D == 3) {
+        const unsigned zj = h ? v1.y : v1.x;
+        t = __hmul2_rn(__hsub2_rn(r2[2], u2h(zj)), hh2[2]);
+        if constexpr (dz != 0) t = __hadd2_rn(t, ccz);
+        acc2 = __hadd2_rn(acc2, __hmul2_rn(t, t));
+      }
+      a[h] = acc2;
+    }
+    acc_nibble(acc, a[0], a[1], thr2);
+    if constexpr (R == R16<D>::CENTRE) {
+      if (ch == selfch) acc &= selfmask;
+    }
+  }
+  return acc >> (4 * (8 - (e - g)));
+}
+
+template <int D, int BT, int PCAP, int WMAX>
+__global__ void __launch_bounds__(BT, D == 3 ? 8 : 8) k_rcll16(SweepArgs a) {
+  constexpr int NR = R16<D>::NR;
+  __shared__ __align__(16) int32_t PK[PCAP + 4];
+  __shared__ unsigned NIB[WMAX * BT];
   __shared__ int s_w[BT / 32];
+  __shared__ int s_tile;
+  __shared__ long long s_base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int r = blockIdx.x * BT + tid;  // row index (particle row0 + r)
+  if (tid == 0) s_tile = (int)(atomicAdd(a.ticket, 1ull) - a.tick0);
+  __syncthreads();
+  const int tile = s_tile;
+  const int r = tile * BT + tid;
   const bool valid = r < a.nrows;
-  const int i = a.row0 + r;
-  const unsigned kw = valid ? (unsigned)__ldg(a.counts + i) : 0u;
-  const int k = (int)(kw & ~kOverflow);
-  const bool retest = (kw & kOverflow) != 0u;
+  const int i = a.row0 + (valid ? r : 0);
+  const char* __restrict__ qc = static_cast<const char*>(a.qc);
+
+  // own particle: coordinates, constants, self record, and its runs
+  __half2 r2[3], hh2[3];
+  const __half2 hc2 = __half2half2(hbits(a.c.h_cc[0])), thr2 = __half2half2(hbits(a.c.h_thr));
+  {
+    const typename Coord<D, FP16>::T o = ldg<typename Coord<D, FP16>::T>(a.pos_own, i);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      r2[k] = k < D ? __half2half2(axis_of<D, FP16>(o, k)) : u2h(0u);
+      hh2[k] = __half2half2(hbits(a.c.h_hh[k]));
+    }
+  }
+  const int self = __ldg(a.selfpos + i);
+  const int selfch = self >> 2;
+  const unsigned selfmask = ~(1u << (28 + (self & 3)));
+  const __half2 ccp_y = row_half2(a.c.h_cc[1], -1, true), ccm_y = row_half2(a.c.h_cc[1], 1, true);
+  const __half2 ccp_z = row_half2(a.c.h_cc[2], -1, true), ccm_z = row_half2(a.c.h_cc[2], 1, true);
+  int cb[NR], ce[NR];
+  {
+    const int nx = a.g.counts[0], ny = a.g.counts[1], nz = a.g.counts[2];
+    const int cx = __ldg(a.cellk[0] + i), cy = __ldg(a.cellk[1] + i);
+    const int cz = D == 3 ? __ldg(a.cellk[2] + i) : 0;
+    const bool ok = valid && cx >= 0 && cx < nx && cy >= 0 && cy < ny && cz >= 0 && cz < nz;
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const int dy = D == 3 ? (q % 3) - 1 : q - 1, dz = D == 3 ? (q / 3) - 1 : 0;
+      int y = cy + dy, z = cz + dz;
+      bool in = ok;
+      if (y < 0) { y += ny; in = in && a.g.wrap[1]; }
+      else if (y >= ny) { y -= ny; in = in && a.g.wrap[1]; }
+      if (D == 3) {
+        if (z < 0) { z += nz; in = in && a.g.wrap[2]; }
+        else if (z >= nz) { z -= nz; in = in && a.g.wrap[2]; }
+      }
+      int2 t = make_int2(0, 0);
+      if (in) t = __ldg(a.tri + ((int64_t)z * ny + y) * nx + cx);
+      cb[q] = t.x;
+      ce[q] = t.y;
+    }
+  }
+
+  // A: hit words
+  int k = 0, w = 0;
+#pragma unroll
+  for (int q = 0; q < NR; ++q) {
+    const int dy = D == 3 ? (q % 3) - 1 : q - 1, dz = D == 3 ? (q / 3) - 1 : 0;
+    const __half2 ccy = dy < 0 ? ccp_y : ccm_y, ccz = dz < 0 ? ccp_z : ccm_z;
+    for (int g = cb[q]; g < ce[q]; g += 8) {
+      unsigned word;
+      switch (q) {  // the row index must be a compile-time constant
+#define RG(Q) case Q: word = r16_group<D, (Q < NR ? Q : 0)>(qc, g, min(g + 8, ce[q]), r2, hh2, hc2, thr2, ccy, ccz, selfch, selfmask); break;
+        RG(0) RG(1) RG(2) RG(3) RG(4) RG(5) RG(6) RG(7) RG(8)
+#undef RG
+        default: word = 0;
+      }
+      k += __popc(word);
+      if (w < WMAX) NIB[w * BT + tid] = word;
+      ++w;
+    }
+  }
+
   const int incl = warp_inclusive_scan(k);
   if (lane == 31) s_w[warp] = incl;
   __syncthreads();
-  int wbase = 0;
-  long long btot = 0;
+  int wbase = 0, btot = 0;
+#pragma unroll
+  for (int u = 0; u < BT / 32; ++u) {
+    wbase += u < warp ? s_w[u] : 0;
+    btot += s_w[u];
+  }
+  const int excl = wbase + incl - k;
+  if (tid == 0) lookback_publish(a.tiles, tile, btot, a.epoch);
+
+  // B: sorted rows. Chunks walked in lockstep, hits appended with predicated
+  // stores; a group whose first id is below the row's last is merged in.
+  const uint4* __restrict__ tags = reinterpret_cast<const uint4*>(a.qtag);
+  auto build = [&](const auto& dst) {
+    int kk = 0, wq = 0;
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const int dy = D == 3 ? (q % 3) - 1 : q - 1, dz = D == 3 ? (q / 3) - 1 : 0;
+      const __half2 ccy = dy < 0 ? ccp_y : ccm_y, ccz = dz < 0 ? ccp_z : ccm_z;
+      for (int g = cb[q]; g < ce[q]; g += 8) {
+        unsigned word;
+        if (wq < WMAX) {
+          word = NIB[wq * BT + tid];
+        } else {
+          switch (q) {
+#define RG(Q) case Q: word = r16_group<D, (Q < NR ? Q : 0)>(qc, g, min(g + 8, ce[q]), r2, hh2, hc2, thr2, ccy, ccz, selfch, selfmask); break;
+            RG(0) RG(1) RG(2) RG(3) RG(4) RG(5) RG(6) RG(7) RG(8)
+#undef RG
+            default: word = 0;
+          }
+        }
+        ++wq;
+        const int gs = kk;
+        for (int ch = g; word; ++ch, word >>= 4) {
+          const unsigned m = word & 15u;
+          if (m) append4(dst, kk, m, __ldg(tags + ch));
+        }
+        if (gs > 0 && kk > gs && dst.ld(gs) < dst.ld(gs - 1)) merge_tail(dst, gs, kk);
+      }
+    }
+  };
+  const bool fits = btot <= PCAP;
+  if (fits && valid && k > 0)
+    build(SharedRow{(uint32_t)__cvta_generic_to_shared(PK) + 4u * (uint32_t)excl});
+
+  if (warp == 0) {
+    const long long b = lookback_resolve(a.tiles, tile, btot, a.epoch);
+    if (lane == 0) s_base = b;
+  }
+  __syncthreads();
+  const long long base = s_base;
+  if (valid) a.offsets[r] = base + excl;
+  if (r == a.nrows - 1) a.offsets[a.nrows] = base + excl + k;
+  if (base + btot > a.capacity) return;
+
+  int32_t* gout = a.items + base;
+  if (!fits) {
+    if (valid && k > 0) build(GlobalRow{gout + excl});
+    return;
+  }
+  stream_tile<BT>(gout, SharedRow{(uint32_t)__cvta_generic_to_shared(PK)}, btot, tid);
+}
+
+// The whole table in one pass over tiles of BT consecutive rows (particle order).
+//   A. each thread tests its particle's candidates; the hit words go to shared
+//      memory (WMAX per thread; later groups are re-tested in B) and the row
+//      length k counts every hit;
+//   block scan of k; the tile publishes its aggregate;
+//   B. rows are built sorted, packed at their final places in a shared tile
+//      (rows longer than the tile buffer go straight to HBM after the look-back);
+//   the look-back resolves the tile's base: offsets[] are written and the tile is
+//      streamed out with 16-byte stores.
+// Tiles are taken in launch order from a ticket counter, so the look-back never
+// waits on a tile that has not started.
+template <int D, int P, int MODE, int BT, int PCAP, int WMAX>
+__global__ void __launch_bounds__(BT) k_sweep(SweepArgs a) {
+  static_assert(BT % 32 == 0 && BT <= 1024, "shape");
+  __shared__ __align__(16) int32_t PK[PCAP + 4];
+  __shared__ unsigned NIB[WMAX * BT];
+  __shared__ int s_w[BT / 32];
+  __shared__ int s_tile;
+  __shared__ long long s_base;
+  using Tst = Tester<D, P, MODE>;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = (int)(atomicAdd(a.ticket, 1ull) - a.tick0);
+  __syncthreads();
+  const int tile = s_tile;
+  const int r = tile * BT + tid;
+  const bool valid = r < a.nrows;
+  const int i = a.row0 + r;
+
+  Tst tst;
+  int selfch = -1;
+  unsigned selfmask = ~0u;
+  int k = 0;
+  if (valid) {
+    tst.init(a, i);
+    const int self = MODE == MODE_ALL ? i : __ldg(a.selfpos + i);
+    selfch = self >> 2;
+    selfmask = ~(1u << (28 + (self & 3)));
+    int w = 0;
+    walk_groups<D, P, MODE>(a, i, tst, [&](const typename Tst::Row& row, bool own, int g, int e) {
+      const unsigned word = group_word<D, P, MODE>(a, tst, row, own, selfch, selfmask, g, e);
+      k += __popc(word);
+      if (w < WMAX) NIB[w * BT + tid] = word;
+      ++w;
+    });
+  }
+
+  const int incl = warp_inclusive_scan(k);
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  int wbase = 0, btot = 0;
 #pragma unroll
   for (int w = 0; w < BT / 32; ++w) {
     wbase += w < warp ? s_w[w] : 0;
     btot += s_w[w];
   }
-  const long long bbase = a.block_sum[blockIdx.x];  // scanned in place by pass 2
-  const long long grow = bbase + wbase + incl - k;
-  if (valid) a.offsets[r] = grow;
-  if (bbase + btot > a.capacity) return;  // device API: the caller grows the table
+  const int excl = wbase + incl - k;
+  if (tid == 0) lookback_publish(a.tiles, tile, btot, a.epoch);
 
-  const int64_t s = MODE == MODE_ALL ? i : (valid ? (int64_t)__ldg(a.rank + i) : 0);
-  const unsigned over = __ballot_sync(0xffffffffu, k > CAP);
-  int32_t* wS = S + warp * 32 * CAP;
-  int32_t* __restrict__ out = a.items + bbase + wbase;
-  if (!over) {
-    const int wrel = incl - k;
-    if (k > 0) {
-      int32_t* row = wS + wrel;
-      build_row<D, P, MODE>(a, i, s, retest, row);
-    }
-    __syncwarp();
-    const int wtot = __shfl_sync(0xffffffffu, incl, 31);
-    for (int e = lane; e < wtot; e += 32) out[e] = wS[e];  // coalesced
+  // B: the sorted row of particle i into dst. Chunks are walked in lockstep and
+  // their hits appended with predicated stores; a group (run) whose first id is
+  // below the row's last one is merged in (rows interleave only where two runs
+  // of different cell rows share id ranges).
+  auto build = [&](const auto& dst) {
+    int kk = 0, w = 0;
+    const uint4* tags = reinterpret_cast<const uint4*>(a.qtag);
+    walk_groups<D, P, MODE>(a, i, tst, [&](const typename Tst::Row& row, bool own, int g, int e) {
+      unsigned word = w < WMAX ? NIB[w * BT + tid]
+                               : group_word<D, P, MODE>(a, tst, row, own, selfch, selfmask, g, e);
+      ++w;
+      const int gs = kk;
+      for (int ch = g; word; ++ch, word >>= 4) {
+        const unsigned m = word & 15u;
+        if (m) append4(dst, kk, m, __ldg(tags + ch));
+      }
+      if (gs > 0 && kk > gs && dst.ld(gs) < dst.ld(gs - 1)) merge_tail(dst, gs, kk);
+    });
+  };
+  const bool fits = btot <= PCAP;
+  if (fits && valid && k > 0)
+    build(SharedRow{(uint32_t)__cvta_generic_to_shared(PK) + 4u * (uint32_t)excl});
+
+  if (warp == 0) {
+    const long long b = lookback_resolve(a.tiles, tile, btot, a.epoch);
+    if (lane == 0) s_base = b;
+  }
+  __syncthreads();
+  const long long base = s_base;
+  if (valid) a.offsets[r] = base + excl;
+  if (r == a.nrows - 1) a.offsets[a.nrows] = base + excl + k;
+  if (base + btot > a.capacity) return;  // device API: the caller grows the table
+
+  int32_t* gout = a.items + base;  // the tile's rows, contiguous
+  if (!fits) {
+    if (valid && k > 0) build(GlobalRow{gout + excl});
     return;
   }
-  // warp with an over-long row: short rows via per-thread slots in shared memory
-  // (one warp-wide store per row), long rows straight into global memory
-  const int wrel = incl - k;
-  if (k > 0) {
-    if (k <= CAP) {
-      int32_t* row = wS + lane * CAP;
-      build_row<D, P, MODE>(a, i, s, retest, row);
-    } else {
-      int32_t* row = out + wrel;
-      build_row<D, P, MODE>(a, i, s, retest, row);
-    }
-  }
-  __syncwarp();
-  for (int w = 0; w < 32; ++w) {
-    const int len = __shfl_sync(0xffffffffu, k, w);
-    const int ro = __shfl_sync(0xffffffffu, wrel, w);
-    if (len > CAP) continue;
-    for (int q = lane; q < len; q += 32) out[ro + q] = wS[w * CAP + q];
-  }
+  stream_tile<BT>(gout, SharedRow{(uint32_t)__cvta_generic_to_shared(PK)}, btot, tid);
 }
 
 // ------------------------------------------------------------------------------
 // Encode
 // ------------------------------------------------------------------------------
-// Own coordinates (particle order); for the cell modes also rank[items[t]] = t
-// and the members' packed coordinates in CSR order. RCLL: src = RelCoords::rel
+// Own coordinates (particle order); for the cell modes also the members' packed coordinates in CSR order. RCLL: src = RelCoords::rel
 // (nnps.cpp:304-315); CLL/all: src = positions (round_coords nnps.cpp:75-89).
 template <int D, int P, int MODE>
 __global__ void k_encode_own(int n, const double* __restrict__ x0, const double* __restrict__ x1,
@@ -760,7 +991,6 @@ __global__ void k_encode_own(int n, const double* __restrict__ x0, const double*
   if constexpr (MODE != MODE_ALL) {
     int j = items[t];
     if (j < 0 || j >= n) j = 0;  // malformed membership: stay memory-safe
-    a.rank[j] = t;
     const double w[3] = {x0[j], D > 1 ? x1[j] : 0.0, D > 2 ? x2[j] : 0.0};
     reinterpret_cast<C*>(pos_csr)[t] = pack<D, P>(w);
     // the cell holding slot t: the member's own cell (RelCoords::cell for RCLL,
@@ -816,9 +1046,10 @@ __device__ __forceinline__ int list_range(const int32_t* st, int tx, int l, int 
   return w;
 }
 
-template <int P>
-__device__ __forceinline__ void store_el(void* q, int64_t r, typename Prec<P>::T v) {
-  reinterpret_cast<typename Prec<P>::T*>(q)[r] = v;
+// record r (chunk r/4, element r%4), quad q
+template <int D, int P, int MODE>
+__device__ __forceinline__ void store_el(void* qc, int64_t r, int q, typename Prec<P>::T v) {
+  *rec_el<D, P, MODE>(qc, r >> 2, q, (int)(r & 3)) = v;
 }
 
 // One thread per cell c: the run's chunk range and the sentinel records (NaN
@@ -845,8 +1076,8 @@ __global__ void k_encode_runs(int64_t C, int nx, int wrapx, const int32_t* __res
   if constexpr (P == FP16) nan = hbits(0x7E00u); else nan = T(NAN);
   for (int q = len; q < 4 * nch; ++q) {
 #pragma unroll
-    for (int k = 0; k < D; ++k) store_el<P>(a.qx[k], slot + q, nan);
-    if constexpr (MODE == MODE_RCLL) store_el<P>(a.qdc, slot + q, T(0.0f));
+    for (int k = 0; k < D; ++k) store_el<D, P, MODE>(a.qc, slot + q, k, nan);
+    if constexpr (MODE == MODE_RCLL) store_el<D, P, MODE>(a.qc, slot + q, D, T(0.0f));
     reinterpret_cast<unsigned*>(a.qtag)[slot + q] = 0xFFFFFFFFu;
   }
 }
@@ -910,9 +1141,9 @@ __global__ void k_encode_members(int n, int nx, int wrapx, PrecConsts pc,
         if constexpr (P == FP16) v = __hadd_rn(v, w > 0 ? sh : __hneg(sh));
         else v = f_add(v, w > 0 ? sh : -sh);
       }
-      store_el<P>(a.qx[k], r, v);
+      store_el<D, P, MODE>(a.qc, r, k, v);
     }
-    if constexpr (MODE == MODE_RCLL) store_el<P>(a.qdc, r, (T)(float)(1 - L));  // dc_x
+    if constexpr (MODE == MODE_RCLL) store_el<D, P, MODE>(a.qc, r, D, (T)(float)(1 - L));  // dc_x
     // output id: the particle index, or its global id for a multi-GPU slab
     reinterpret_cast<unsigned*>(a.qtag)[r] = a.ids ? (unsigned)__ldg(a.ids + j) : (unsigned)j;
     if (L == 1) a.selfpos[j] = (int)r;
@@ -950,30 +1181,41 @@ __global__ void k_encode_all(int n, const void* __restrict__ pos_own, SweepArgs 
     if (u == 0) qt.x = tag; else if (u == 1) qt.y = tag; else if (u == 2) qt.z = tag; else qt.w = tag;
   }
 #pragma unroll
-  for (int k = 0; k < D; ++k) reinterpret_cast<Q*>(a.qx[k])[ch] = qx[k];
+  for (int k = 0; k < D; ++k)
+    *reinterpret_cast<Q*>(rec_el<D, P, MODE_ALL>(a.qc, ch, k, 0)) = qx[k];
   reinterpret_cast<uint4*>(a.qtag)[ch] = qt;
 }
 
 template <int D>
 struct Shape {
-  static constexpr int CBT = 128;               // count: threads per block
-  static constexpr int BT = D == 3 ? 64 : 128;  // fill: rows per block (= scan tile)
-  static constexpr int CAP = D == 3 ? 96 : 32;  // fill: shared-memory slots per row
+  static constexpr int BT = D == 3 ? 64 : 128;                     // rows per tile
+  static constexpr int PCAP = D == 3 ? 64 * 64 : (D == 2 ? 128 * 24 : 128 * 8);  // packed tile
+  static constexpr int WMAX = D == 3 ? 24 : (D == 2 ? 8 : 4);      // hit words kept per row
 };
 
 // ------------------------------------------------------------------------------
 // Host-side launchers (called from capi.cu)
 // ------------------------------------------------------------------------------
-int fill_tile(int dim) { return dim == 3 ? Shape<3>::BT : Shape<2>::BT; }
-int mask_words(int dim) {
-  return dim == 3 ? MaskWords<3>::W : (dim == 2 ? MaskWords<2>::W : MaskWords<1>::W);
-}
+int sweep_tile(int dim) { return dim == 3 ? Shape<3>::BT : Shape<2>::BT; }
 size_t coord_bytes(int dim, int prec) {
   if (prec == FP16) return dim == 3 ? 8 : 4;
   if (prec == FP32) return dim == 1 ? 4 : (dim == 2 ? 8 : 16);
   return dim == 1 ? 8 : (dim == 2 ? 16 : 32);
 }
-size_t quad_bytes(int prec) { return prec == FP16 ? 8 : (prec == FP32 ? 16 : 32); }
+size_t chunk_bytes(int dim, int prec, int mode) {
+#define CB(D, P, M) if (dim == D && prec == P && mode == M) return ChunkLay<D, P, M>::BYTES;
+  CB(1, FP16, MODE_RCLL) CB(2, FP16, MODE_RCLL) CB(3, FP16, MODE_RCLL)
+  CB(1, FP32, MODE_RCLL) CB(2, FP32, MODE_RCLL) CB(3, FP32, MODE_RCLL)
+  CB(1, FP64, MODE_RCLL) CB(2, FP64, MODE_RCLL) CB(3, FP64, MODE_RCLL)
+  CB(1, FP16, MODE_CLL) CB(2, FP16, MODE_CLL) CB(3, FP16, MODE_CLL)
+  CB(1, FP32, MODE_CLL) CB(2, FP32, MODE_CLL) CB(3, FP32, MODE_CLL)
+  CB(1, FP64, MODE_CLL) CB(2, FP64, MODE_CLL) CB(3, FP64, MODE_CLL)
+  CB(1, FP16, MODE_ALL) CB(2, FP16, MODE_ALL) CB(3, FP16, MODE_ALL)
+  CB(1, FP32, MODE_ALL) CB(2, FP32, MODE_ALL) CB(3, FP32, MODE_ALL)
+  CB(1, FP64, MODE_ALL) CB(2, FP64, MODE_ALL) CB(3, FP64, MODE_ALL)
+#undef CB
+  return 0;
+}
 // chunks the candidate arrays need
 int64_t chunk_capacity(int mode, int64_t n, int64_t C) {
   return mode == MODE_ALL ? (n + 3) / 4 + 1 : (3 * n + 6 * C) / 4 + 2;
@@ -1023,19 +1265,13 @@ int launch_encode(int dim, int prec, int mode, int n, int64_t C, int nx, int wra
 }
 
 template <int D, int P, int M>
-static void count_t(const SweepArgs& a, cudaStream_t st) {
-  constexpr int CBT = Shape<D>::CBT;
-  k_count<D, P, M, CBT><<<(a.n + CBT - 1) / CBT, CBT, 0, st>>>(a);
-  const int tile = Shape<D>::BT;
-  const int nt = (a.nrows + tile - 1) / tile;
-  k_tile_sums<<<nt, 256, 0, st>>>(a.counts + a.row0, a.nrows, tile, a.block_sum);
-  k_scan_blocks<<<1, 1024, 0, st>>>(a.block_sum, nt, a.offsets, a.nrows);
-}
-
-template <int D, int P, int M>
-static void fill_t(const SweepArgs& a, cudaStream_t st) {
-  constexpr int BT = Shape<D>::BT;
-  k_fill<D, P, M, BT, Shape<D>::CAP><<<(a.nrows + BT - 1) / BT, BT, 0, st>>>(a);
+static void sweep_t(const SweepArgs& a, cudaStream_t st) {
+  using S = Shape<D>;
+  const unsigned nb = (unsigned)((a.nrows + S::BT - 1) / S::BT);
+  if constexpr (P == FP16 && M == MODE_RCLL && D >= 2)
+    k_rcll16<D, S::BT, S::PCAP, S::WMAX><<<nb, S::BT, 0, st>>>(a);
+  else
+    k_sweep<D, P, M, S::BT, S::PCAP, S::WMAX><<<nb, S::BT, 0, st>>>(a);
 }
 
 #define SW(FN, D, P, M) \
@@ -1046,10 +1282,8 @@ static void fill_t(const SweepArgs& a, cudaStream_t st) {
   SWP(FN, 1, MODE_CLL) SWP(FN, 2, MODE_CLL) SWP(FN, 3, MODE_CLL)    \
   SWP(FN, 1, MODE_ALL) SWP(FN, 2, MODE_ALL) SWP(FN, 3, MODE_ALL)
 
-// Pass 1 + 2: counts and hit nibbles, tile sums, scanned tile bases, offsets[n].
-void launch_count(int dim, int prec, int mode, const SweepArgs& a, cudaStream_t st) { SWA(count_t) }
-// Pass 3: offsets[0..n) and the rows.
-void launch_fill(int dim, int prec, int mode, const SweepArgs& a, cudaStream_t st) { SWA(fill_t) }
+// The single-pass sweep: offsets[0..nrows] and the rows.
+void launch_sweep(int dim, int prec, int mode, const SweepArgs& a, cudaStream_t st) { SWA(sweep_t) }
 
 #undef SWA
 #undef SWP

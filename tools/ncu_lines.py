@@ -9,7 +9,8 @@ from collections import defaultdict
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source",
+kfilter = sys.argv[3:4]
+txt = subprocess.run(["ncu", "-i", rep] + (["-k", "regex:" + kfilter[0]] if kfilter else []) + ["--page", "source", "--csv", "--print-source",
                       "cuda,sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
 agg = defaultdict(lambda: [0, 0, ""])

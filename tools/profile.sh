@@ -10,7 +10,7 @@ shift
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches_${TAG}.csv \
     python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 "$@" > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_(count|fill|encode_members|encode_runs)" -s 12 -c 4 \
+ncu --set full --clock-control none --import-source on -k regex:"k_(sweep|encode_members)" -s 8 -c 2 \
     -o gpurun_out/prof_${TAG} \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 "$@" \
     > gpurun_out/ncu_${TAG}.log 2>&1

@@ -1,0 +1,26 @@
+#!/bin/bash
+# Quick GPU iteration (under gpurun): C2 and C3 bench lines and one ncu --set full
+# capture of k_sweep.   tools/quick.sh <tag> [--tests] [--no-ncu]
+TAG=$1; shift
+mkdir -p gpurun_out
+for a in "$@"; do
+  [ "$a" = "--tests" ] && { timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_${TAG}.log 2>&1; tail -3 gpurun_out/pytest_${TAG}.log; }
+done
+for C in C2 C3; do
+  python bench.py --config $C --no-cpu-baseline --e2e-steps 2 > gpurun_out/bench_${TAG}_${C}.json 2> gpurun_out/bench_${TAG}_${C}.err
+  python - "$TAG" "$C" <<'PY'
+import json, sys
+t, c = sys.argv[1], sys.argv[2]
+try:
+    d = json.load(open(f"gpurun_out/bench_{t}_{c}.json"))
+    print(c, "value", f"{d['value']:.4g}", {k: round(v * 1e3, 1) for k, v in d["breakdown_ms"].items()},
+          "frac", round(d["roofline"]["frac"], 4), "parity", d["parity"]["bit_exact_vs_reference_hash"])
+except Exception as e:
+    print(c, "bench failed", e, open(f"gpurun_out/bench_{t}_{c}.err").read()[-1500:])
+PY
+done
+case " $* " in *" --no-ncu "*) exit 0;; esac
+ncu --set full --clock-control none --import-source on -k regex:"k_(sweep|rcll16)" -s 4 -c 1 \
+    -o gpurun_out/prof_${TAG} python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 \
+    > gpurun_out/ncu_${TAG}.log 2>&1
+tail -1 gpurun_out/ncu_${TAG}.log
