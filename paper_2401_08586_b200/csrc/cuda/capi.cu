@@ -21,11 +21,11 @@ int launch_encode(int dim, int prec, int mode, int n, int64_t C, int nx, int wra
                   const PrecConsts& pc, const double* const x[3], const int32_t* items,
                   const int32_t* start, void* pos_csr, int32_t* cell_slot, const SweepArgs& a,
                   cudaStream_t st);
-void launch_sweep(int dim, int prec, int mode, const SweepArgs& a, cudaStream_t st);
+int64_t launch_sweep(int dim, int prec, int mode, const SweepArgs& a, cudaStream_t st);
 size_t coord_bytes(int dim, int prec);
 size_t chunk_bytes(int dim, int prec, int mode);
 int64_t chunk_capacity(int mode, int64_t n, int64_t C);
-int sweep_tile(int dim);
+int sweep_tile(int dim, int prec, int mode);
 // binning.cu
 int64_t scan_tiles(int64_t C);
 void launch_locate(int mode, const LocateArgs& a, cudaStream_t st);
@@ -345,7 +345,7 @@ int run_sweep(sphx_context* ctx, int dim, int prec, int mode, SweepArgs& a, int3
               int64_t capacity) {
   if (a.n == 0 || a.nrows == 0) return SPHX_OK;
   cudaStream_t st = ctx->stream;
-  const int64_t nt = (a.nrows + sweep_tile(dim) - 1) / sweep_tile(dim);
+  const int64_t nt = (a.nrows + sweep_tile(dim, prec, mode) - 1) / sweep_tile(dim, prec, mode);
   if (nt > ctx->sw_ntiles || ctx->sw_epoch >= 0xFFFFu) {
     // fresh (or recycled) look-back words: epoch 0 marks them unpublished
     TRY(ctx->sw_tiles.ensure(sizeof(unsigned long long) * std::max<int64_t>(nt, ctx->sw_ntiles)));
@@ -364,9 +364,9 @@ int run_sweep(sphx_context* ctx, int dim, int prec, int mode, SweepArgs& a, int3
   a.ticket = ctx->sw_ticket.as<unsigned long long>();
   a.tick0 = ctx->sw_tick;
   a.epoch = ++ctx->sw_epoch;
-  launch_sweep(dim, prec, mode, a, st);
+  const int64_t used = launch_sweep(dim, prec, mode, a, st);
   CKL();
-  ctx->sw_tick += (unsigned long long)nt;
+  ctx->sw_tick += (unsigned long long)used;
   ++ctx->launches;
   if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], st));
   return SPHX_OK;

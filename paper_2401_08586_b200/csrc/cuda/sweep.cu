@@ -569,6 +569,11 @@ struct SharedRow {
   __device__ __forceinline__ void st(int e, int v) const {
     asm volatile("st.shared.b32 [%0], %1;" ::"r"(base + 4u * (uint32_t)e), "r"(v) : "memory");
   }
+  // predicated store (no branch)
+  __device__ __forceinline__ void st_if(bool c, int e, int v) const {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p st.shared.b32 [%0], %1;\n\t}"
+                 ::"r"(base + 4u * (uint32_t)e), "r"(v), "r"((int)c) : "memory");
+  }
   __device__ __forceinline__ int ld(int e) const {
     int v;
     asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(base + 4u * (uint32_t)e) : "memory");
@@ -578,6 +583,9 @@ struct SharedRow {
 struct GlobalRow {
   int32_t* p;
   __device__ __forceinline__ void st(int e, int v) const { p[e] = v; }
+  __device__ __forceinline__ void st_if(bool c, int e, int v) const {
+    if (c) p[e] = v;
+  }
   __device__ __forceinline__ int ld(int e) const { return p[e]; }
 };
 
@@ -588,10 +596,10 @@ __device__ __forceinline__ void append4(const Row& dst, int& k, unsigned m, cons
   const int p1 = k + (int)(m & 1u);
   const int p2 = p1 + (int)((m >> 1) & 1u);
   const int p3 = p2 + (int)((m >> 2) & 1u);
-  if (m & 1u) dst.st(k, (int)tq.x);
-  if (m & 2u) dst.st(p1, (int)tq.y);
-  if (m & 4u) dst.st(p2, (int)tq.z);
-  if (m & 8u) dst.st(p3, (int)tq.w);
+  dst.st_if(m & 1u, k, (int)tq.x);
+  dst.st_if(m & 2u, p1, (int)tq.y);
+  dst.st_if(m & 4u, p2, (int)tq.z);
+  dst.st_if(m & 8u, p3, (int)tq.w);
   k = p3 + (int)(m >> 3);
 }
 
@@ -648,7 +656,7 @@ __device__ __forceinline__ long long lookback_resolve(unsigned long long* tiles,
   const int lane = threadIdx.x & 31;
   long long excl = 0;
   int p = bid - 1;
-  unsigned backoff = 64;
+  unsigned backoff = 64, spins = 0;
   while (true) {
     const int idx = p - lane;
     const unsigned long long st = idx >= 0 ? ld_acquire_u64(&tiles[idx]) : (E | PRE);
@@ -658,6 +666,9 @@ __device__ __forceinline__ long long lookback_resolve(unsigned long long* tiles,
     const int first = pre_mask ? __ffs(pre_mask) - 1 : 32;
     const unsigned need = first >= 31 ? 0xffffffffu : ((2u << first) - 1u);
     if (zero_mask & need) {
+      // a predecessor that never publishes is a bug: fail the launch (~4 s)
+      // instead of hanging the device
+      if (++spins > (1u << 22)) __trap();
       __nanosleep(backoff);
       backoff = backoff < 1024 ? backoff * 2 : 1024;
       continue;
@@ -683,60 +694,82 @@ __device__ __forceinline__ long long lookback_resolve(unsigned long long* tiles,
 template <int D>
 struct R16 {
   static constexpr int NR = D == 3 ? 9 : 3;  // runs per particle
-  static constexpr int CENTRE = NR / 2;      // dy = dz = 0
 };
 
-template <int D, int R>
-__device__ __forceinline__ unsigned r16_group(const char* __restrict__ qc, int g, int e,
-                                              const __half2 (&r2)[3], const __half2 (&hh2)[3],
-                                              __half2 hc2, __half2 thr2, __half2 ccy, __half2 ccz,
-                                              int selfch, unsigned selfmask) {
-  constexpr int dy = D == 3 ? (R % 3) - 1 : R - 1;
-  constexpr int dz = D == 3 ? (R / 3) - 1 : 0;
-  unsigned acc = 0;
-#pragma unroll 4
-  for (int ch = g; ch < e; ++ch) {
-    const uint4* p = reinterpret_cast<const uint4*>(qc + (size_t)ch * 32);
-    const uint4 v0 = __ldg(p);
-    uint4 v1;
-    if constexpr (D == 3) v1 = __ldg(p + 1);
-    else {
-      const uint2 t = __ldg(reinterpret_cast<const uint2*>(p + 1));
-      v1 = make_uint4(t.x, t.y, 0u, 0u);
-    }
-    // quads: x = (v0.x, v0.y), y = (v0.z, v0.w), 3-D z = (v1.x, v1.y), dc = last quad
-    const unsigned dcl = D == 3 ? v1.z : v1.x, dch = D == 3 ? v1.w : v1.y;
-    __half2 a[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const unsigned xj = h ? v0.y : v0.x, yj = h ? v0.w : v0.z;
-      __half2 t = __hmul2_rn(__hsub2_rn(r2[0], u2h(xj)), hh2[0]);
-      __half2 d = __hfma2(u2h(h ? dch : dcl), hc2, t);
-      __half2 acc2 = __hmul2_rn(d, d);
-      t = __hmul2_rn(__hsub2_rn(r2[1], u2h(yj)), hh2[1]);
-      if constexpr (dy != 0) t = __hadd2_rn(t, ccy);
-      acc2 = __hadd2_rn(acc2, __hmul2_rn(t, t));
-      if constexpr (D == 3) {
-        const unsigned zj = h ? v1.y : v1.x;
-        t = __hmul2_rn(__hsub2_rn(r2[2], u2h(zj)), hh2[2]);
-        if constexpr (dz != 0) t = __hadd2_rn(t, ccz);
-        acc2 = __hadd2_rn(acc2, __hmul2_rn(t, t));
-      }
-      a[h] = acc2;
-    }
-    acc_nibble(acc, a[0], a[1], thr2);
-    if constexpr (R == R16<D>::CENTRE) {
-      if (ch == selfch) acc &= selfmask;
-    }
+// One chunk (4 candidates) against particle i: the 4-bit hit nibble is shifted
+// into acc from the top (acc = acc >> 4 | nibble << 28).
+template <int D>
+__device__ __forceinline__ void r16_chunk(const char* __restrict__ qc, int ch, const __half2 (&r2)[3],
+                                          const __half2 (&hh2)[3], __half2 hc2, __half2 thr2,
+                                          __half2 ccy, __half2 ccz, unsigned& acc) {
+  const uint4* p = reinterpret_cast<const uint4*>(qc + (size_t)ch * 32);
+  const uint4 v0 = __ldg(p);
+  uint4 v1;
+  if constexpr (D == 3) {
+    v1 = __ldg(p + 1);
+  } else {
+    const uint2 t = __ldg(reinterpret_cast<const uint2*>(p + 1));
+    v1 = make_uint4(t.x, t.y, 0u, 0u);
   }
-  return acc >> (4 * (8 - (e - g)));
+  // quads: x = (v0.x, v0.y), y = (v0.z, v0.w), 3-D z = (v1.x, v1.y), dc = last quad
+  const unsigned dcl = D == 3 ? v1.z : v1.x, dch = D == 3 ? v1.w : v1.y;
+  __half2 a[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const unsigned xj = h ? v0.y : v0.x, yj = h ? v0.w : v0.z;
+    __half2 t = __hmul2_rn(__hsub2_rn(r2[0], u2h(xj)), hh2[0]);
+    const __half2 d = __hfma2(u2h(h ? dch : dcl), hc2, t);
+    __half2 acc2 = __hmul2_rn(d, d);
+    t = __hadd2_rn(__hmul2_rn(__hsub2_rn(r2[1], u2h(yj)), hh2[1]), ccy);
+    acc2 = __hadd2_rn(acc2, __hmul2_rn(t, t));
+    if constexpr (D == 3) {
+      const unsigned zj = h ? v1.y : v1.x;
+      t = __hadd2_rn(__hmul2_rn(__hsub2_rn(r2[2], u2h(zj)), hh2[2]), ccz);
+      acc2 = __hadd2_rn(acc2, __hmul2_rn(t, t));
+    }
+    a[h] = acc2;
+  }
+  acc_nibble(acc, a[0], a[1], thr2);
 }
 
+// Cursor over a particle's runs, flattened into one chunk sequence. The run
+// table holds the non-empty runs of the particle as {first chunk | row << 27,
+// end chunk}; the row (dz, dy) gives the y / z centre differences.
+struct RunCursor {
+  int r, ch, end;
+  __half2 ccy, ccz;
+};
+
+// row constants: cc(-1) = +hc16 (dc = -dy), cc(0) = 0, cc(+1) = -hc16, as half2 bits
+__device__ __forceinline__ __half2 cc_of(unsigned hc16, int off) {
+  const unsigned b = off < 0 ? hc16 : (hc16 ^ 0x8000u);
+  return u2h(off == 0 ? 0u : (b | (b << 16)));
+}
+
+template <int D, int BT>
+__device__ __forceinline__ void run_open(const int2* runs, int tid, int r, RunCursor& c,
+                                         unsigned hcy, unsigned hcz) {
+  const int2 e = runs[r * BT + tid];
+  const int q = (unsigned)e.x >> 27;  // 0..8: dy = q % 3 - 1, dz = q / 3 - 1
+  c.r = r;
+  c.ch = e.x & ((1 << 27) - 1);
+  c.end = e.y;
+  c.ccy = cc_of(hcy, q % 3 - 1);
+  c.ccz = cc_of(hcz, q / 3 - 1);
+}
+
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+// Tiles of BT consecutive rows (one block each): A (hit words) -> block scan ->
+// publish -> B (sorted rows into the packed tile) -> resolve -> offsets, stream.
 template <int D, int BT, int PCAP, int WMAX>
-__global__ void __launch_bounds__(BT, D == 3 ? 8 : 8) k_rcll16(SweepArgs a) {
+__global__ void __launch_bounds__(BT, D == 3 ? 12 : 8) k_rcll16(SweepArgs a) {
   constexpr int NR = R16<D>::NR;
   __shared__ __align__(16) int32_t PK[PCAP + 4];
   __shared__ unsigned NIB[WMAX * BT];
+  __shared__ int2 RUNS[NR * BT];
   __shared__ int s_w[BT / 32];
   __shared__ int s_tile;
   __shared__ long long s_base;
@@ -748,9 +781,11 @@ __global__ void __launch_bounds__(BT, D == 3 ? 8 : 8) k_rcll16(SweepArgs a) {
   const bool valid = r < a.nrows;
   const int i = a.row0 + (valid ? r : 0);
   const char* __restrict__ qc = static_cast<const char*>(a.qc);
+  const uint4* __restrict__ tags = reinterpret_cast<const uint4*>(a.qtag);
 
-  // own particle: coordinates, constants, self record, and its runs
+  // own particle: coordinates, constants, self record
   __half2 r2[3], hh2[3];
+  const unsigned hcy = a.c.h_cc[1], hcz = a.c.h_cc[2];
   const __half2 hc2 = __half2half2(hbits(a.c.h_cc[0])), thr2 = __half2half2(hbits(a.c.h_thr));
   {
     const typename Coord<D, FP16>::T o = ldg<typename Coord<D, FP16>::T>(a.pos_own, i);
@@ -763,9 +798,9 @@ __global__ void __launch_bounds__(BT, D == 3 ? 8 : 8) k_rcll16(SweepArgs a) {
   const int self = __ldg(a.selfpos + i);
   const int selfch = self >> 2;
   const unsigned selfmask = ~(1u << (28 + (self & 3)));
-  const __half2 ccp_y = row_half2(a.c.h_cc[1], -1, true), ccm_y = row_half2(a.c.h_cc[1], 1, true);
-  const __half2 ccp_z = row_half2(a.c.h_cc[2], -1, true), ccm_z = row_half2(a.c.h_cc[2], 1, true);
-  int cb[NR], ce[NR];
+
+  // the particle's non-empty runs, (dz, dy) ascending
+  int nruns = 0;
   {
     const int nx = a.g.counts[0], ny = a.g.counts[1], nz = a.g.counts[2];
     const int cx = __ldg(a.cellk[0] + i), cy = __ldg(a.cellk[1] + i);
@@ -773,7 +808,7 @@ __global__ void __launch_bounds__(BT, D == 3 ? 8 : 8) k_rcll16(SweepArgs a) {
     const bool ok = valid && cx >= 0 && cx < nx && cy >= 0 && cy < ny && cz >= 0 && cz < nz;
 #pragma unroll
     for (int q = 0; q < NR; ++q) {
-      const int dy = D == 3 ? (q % 3) - 1 : q - 1, dz = D == 3 ? (q / 3) - 1 : 0;
+      const int dy = (q % 3) - 1, dz = D == 3 ? (q / 3) - 1 : 0;
       int y = cy + dy, z = cz + dz;
       bool in = ok;
       if (y < 0) { y += ny; in = in && a.g.wrap[1]; }
@@ -782,29 +817,34 @@ __global__ void __launch_bounds__(BT, D == 3 ? 8 : 8) k_rcll16(SweepArgs a) {
         if (z < 0) { z += nz; in = in && a.g.wrap[2]; }
         else if (z >= nz) { z -= nz; in = in && a.g.wrap[2]; }
       }
-      int2 t = make_int2(0, 0);
-      if (in) t = __ldg(a.tri + ((int64_t)z * ny + y) * nx + cx);
-      cb[q] = t.x;
-      ce[q] = t.y;
+      if (in) {
+        const int2 t = __ldg(a.tri + ((int64_t)z * ny + y) * nx + cx);
+        if (t.y > t.x) {
+          RUNS[nruns * BT + tid] = make_int2(t.x | ((D == 3 ? q : q + 3) << 27), t.y);
+          ++nruns;
+        }
+      }
     }
   }
 
-  // A: hit words
+  // A: hit words. Each run is tested in groups of up to 8 chunks (one word); the
+  // id quads of chunks with hits are prefetched into L1 for B.
   int k = 0, w = 0;
-#pragma unroll
-  for (int q = 0; q < NR; ++q) {
-    const int dy = D == 3 ? (q % 3) - 1 : q - 1, dz = D == 3 ? (q / 3) - 1 : 0;
-    const __half2 ccy = dy < 0 ? ccp_y : ccm_y, ccz = dz < 0 ? ccp_z : ccm_z;
-    for (int g = cb[q]; g < ce[q]; g += 8) {
-      unsigned word;
-      switch (q) {  // the row index must be a compile-time constant
-#define RG(Q) case Q: word = r16_group<D, (Q < NR ? Q : 0)>(qc, g, min(g + 8, ce[q]), r2, hh2, hc2, thr2, ccy, ccz, selfch, selfmask); break;
-        RG(0) RG(1) RG(2) RG(3) RG(4) RG(5) RG(6) RG(7) RG(8)
-#undef RG
-        default: word = 0;
+  for (int q = 0; q < nruns; ++q) {
+    RunCursor c;
+    run_open<D, BT>(RUNS, tid, q, c, hcy, hcz);
+    for (int g = c.ch; g < c.end; g += 8) {
+      const int e = min(g + 8, c.end);
+      unsigned acc = 0;
+#pragma unroll 4
+      for (int ch = g; ch < e; ++ch) {
+        r16_chunk<D>(qc, ch, r2, hh2, hc2, thr2, c.ccy, c.ccz, acc);
+        if (ch == selfch) acc &= selfmask;
+        if (acc >> 28) prefetch_l1(tags + ch);
       }
-      k += __popc(word);
-      if (w < WMAX) NIB[w * BT + tid] = word;
+      acc >>= 4 * (8 - (e - g));
+      k += __popc(acc);
+      if (w < WMAX) NIB[w * BT + tid] = acc;
       ++w;
     }
   }
@@ -821,35 +861,35 @@ __global__ void __launch_bounds__(BT, D == 3 ? 8 : 8) k_rcll16(SweepArgs a) {
   const int excl = wbase + incl - k;
   if (tid == 0) lookback_publish(a.tiles, tile, btot, a.epoch);
 
-  // B: sorted rows. Chunks walked in lockstep, hits appended with predicated
-  // stores; a group whose first id is below the row's last is merged in.
-  const uint4* __restrict__ tags = reinterpret_cast<const uint4*>(a.qtag);
+  // B: sorted rows, hits appended with predicated stores; a run whose first id
+  // is below the row's last is merged in (runs interleave only where two cell
+  // rows share id ranges).
   auto build = [&](const auto& dst) {
     int kk = 0, wq = 0;
-#pragma unroll
-    for (int q = 0; q < NR; ++q) {
-      const int dy = D == 3 ? (q % 3) - 1 : q - 1, dz = D == 3 ? (q / 3) - 1 : 0;
-      const __half2 ccy = dy < 0 ? ccp_y : ccm_y, ccz = dz < 0 ? ccp_z : ccm_z;
-      for (int g = cb[q]; g < ce[q]; g += 8) {
+    for (int q = 0; q < nruns; ++q) {
+      RunCursor c;
+      run_open<D, BT>(RUNS, tid, q, c, hcy, hcz);
+      const int gs = kk;
+      for (int g = c.ch; g < c.end; g += 8) {
         unsigned word;
         if (wq < WMAX) {
           word = NIB[wq * BT + tid];
-        } else {
-          switch (q) {
-#define RG(Q) case Q: word = r16_group<D, (Q < NR ? Q : 0)>(qc, g, min(g + 8, ce[q]), r2, hh2, hc2, thr2, ccy, ccz, selfch, selfmask); break;
-            RG(0) RG(1) RG(2) RG(3) RG(4) RG(5) RG(6) RG(7) RG(8)
-#undef RG
-            default: word = 0;
+        } else {  // not kept: test again
+          const int e = min(g + 8, c.end);
+          word = 0;
+          for (int ch = g; ch < e; ++ch) {
+            r16_chunk<D>(qc, ch, r2, hh2, hc2, thr2, c.ccy, c.ccz, word);
+            if (ch == selfch) word &= selfmask;
           }
+          word >>= 4 * (8 - (e - g));
         }
         ++wq;
-        const int gs = kk;
         for (int ch = g; word; ++ch, word >>= 4) {
           const unsigned m = word & 15u;
           if (m) append4(dst, kk, m, __ldg(tags + ch));
         }
-        if (gs > 0 && kk > gs && dst.ld(gs) < dst.ld(gs - 1)) merge_tail(dst, gs, kk);
       }
+      if (gs > 0 && kk > gs && dst.ld(gs) < dst.ld(gs - 1)) merge_tail(dst, gs, kk);
     }
   };
   const bool fits = btot <= PCAP;
@@ -1196,7 +1236,9 @@ struct Shape {
 // ------------------------------------------------------------------------------
 // Host-side launchers (called from capi.cu)
 // ------------------------------------------------------------------------------
-int sweep_tile(int dim) { return dim == 3 ? Shape<3>::BT : Shape<2>::BT; }
+int sweep_tile(int dim, int prec, int mode) {
+  return dim == 3 ? Shape<3>::BT : Shape<2>::BT;
+}
 size_t coord_bytes(int dim, int prec) {
   if (prec == FP16) return dim == 3 ? 8 : 4;
   if (prec == FP32) return dim == 1 ? 4 : (dim == 2 ? 8 : 16);
@@ -1221,15 +1263,319 @@ int64_t chunk_capacity(int mode, int64_t n, int64_t C) {
   return mode == MODE_ALL ? (n + 3) / 4 + 1 : (3 * n + 6 * C) / 4 + 2;
 }
 
+// ------------------------------------------------------------------------------
+// Row-tiled encode (RCLL / CLL): one CTA per XB consecutive cells of one cell row
+// (the x-fastest linear cell index makes the row's slots and its runs contiguous).
+//   1. the member window -- cells [x0-2, x1+2) -- is staged in shared memory: merge
+//      key (id, or global id of a slab), CSR id and coordinates at storage precision
+//      (RelCoords::rel for RCLL, positions for CLL; round_to, nnps.cpp:304-315/75-89);
+//   2. each member of cells [x0-1, x1] is placed in the runs centred at x-1, x, x+1
+//      that this CTA owns: its position is its index in its cell plus the number of
+//      smaller keys in the run's two other cells (binary search; cells hold ascending
+//      keys), i.e. its place in the id-merge of the three cells;
+//   3. the CTA's runs -- a contiguous chunk range -- are assembled in shared memory
+//      (sentinels: NaN coordinates, id ~0) and written out with 16-byte stores.
+// Own-cell members also get pos_own (particle order) and selfpos. The candidate's
+// cell is its CSR cell and its x offset dc = 1 - list (nnps.cpp:359-362); CLL
+// records of a wrapped list carry round_to(prec, x + shift) (nnps.cpp:116).
+// ------------------------------------------------------------------------------
+struct EncArgs {
+  int nx, nxb, wrapx;
+  int64_t nrows;               // cell rows (ny * nz)
+  const int32_t* start;        // CellGrid::cell_start
+  const int32_t* items;        // CellGrid::items
+  const double* x[3];          // rel (RCLL) or positions (CLL)
+  PrecConsts pc;
+};
+
+template <int D, int P>
+struct EncShape {
+  static constexpr int XB = D == 3 ? 32 : 64;       // cells per CTA
+  static constexpr int BT = 256;
+  static constexpr int WCAP = D == 3 ? 1024 : 768;  // staged window members
+  static constexpr int OCAP = D == 3 ? 512 : 384;   // staged chunks
+};
+
+// window: key, id (int32), coordinates; then the chunks and their ids
+template <int D, int P, int MODE>
+constexpr size_t enc_smem_bytes() {
+  using E = EncShape<D, P>;
+  using L = ChunkLay<D, P, MODE>;
+  return (size_t)E::WCAP * (8 + D * sizeof(typename Prec<P>::T)) + (size_t)E::OCAP * (L::BYTES + 16);
+}
+
+template <int D, int P, int MODE>
+__global__ void __launch_bounds__(EncShape<D, P>::BT) k_encode_rows(EncArgs e, SweepArgs a) {
+  using E = EncShape<D, P>;
+  using L = ChunkLay<D, P, MODE>;
+  using T = typename Prec<P>::T;
+  constexpr int XB = E::XB, BT = E::BT, NW = XB + 4;
+  extern __shared__ __align__(16) unsigned char sm[];
+  int32_t* skey = reinterpret_cast<int32_t*>(sm);
+  int32_t* sid = skey + E::WCAP;
+  T* scrd = reinterpret_cast<T*>(sid + E::WCAP);                 // [D][WCAP]
+  unsigned char* sch = sm + (size_t)E::WCAP * (8 + D * sizeof(T));  // [OCAP][BYTES]
+  uint32_t* stag = reinterpret_cast<uint32_t*>(sch + (size_t)E::OCAP * L::BYTES);  // [OCAP*4]
+  __shared__ int wst[NW + 1];   // window member offset of local cell u
+  __shared__ int wgs[NW];       // CSR slot of local cell u's first member
+  __shared__ int wraw[NW];      // unwrapped x of local cell u
+  __shared__ int64_t s_ch0;     // first chunk of the CTA's runs
+  __shared__ int s_nch;         // chunks of the CTA's runs
+
+  const int tid = threadIdx.x;
+  const int64_t row = blockIdx.x / e.nxb;
+  const int x0 = (int)(blockIdx.x % e.nxb) * XB;
+  const int x1 = min(x0 + XB, e.nx);
+  const int nx = e.nx;
+  const int32_t* st = e.start + row * nx;  // st[nx] is the next row's first slot
+  const int64_t crow = row * nx;
+
+  // window cells (count and first slot), prefix over them by warp 0
+  __shared__ int64_t rslot[XB];  // first record of each run owned here
+  if (tid < 32) {
+    int tot = 0;
+    for (int u0 = 0; u0 < NW; u0 += 32) {
+      const int u = u0 + tid;
+      int cnt = 0;
+      if (u < NW) {
+        int gx = x0 - 2 + u, gs = 0;
+        wraw[u] = gx;
+        bool ok = gx >= 0 && gx < nx;
+        if (!ok && e.wrapx) {
+          gx = ((gx % nx) + nx) % nx;
+          ok = true;
+        }
+        if (ok) {
+          gs = st[gx];
+          cnt = st[gx + 1] - gs;
+        }
+        wgs[u] = gs;
+      }
+      const int incl = warp_inclusive_scan(cnt);
+      if (u < NW) wst[u + 1] = tot + incl;
+      tot += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (tid == 0) wst[0] = 0;
+  }
+  for (int v = tid; v < x1 - x0; v += BT)
+    rslot[v] = run_record_slot(st, x0 + v, nx, e.wrapx, crow + x0 + v);
+  __syncthreads();
+  const int W = wst[NW];
+  const bool win_sm = W <= E::WCAP;
+
+  // member window: key, id, coordinates
+  auto member = [&](int m, int& u) {
+    int lo = 0, hi = NW;  // last u with wst[u] <= m
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (wst[mid] <= m) lo = mid; else hi = mid;
+    }
+    u = lo;
+    return __ldg(e.items + wgs[lo] + (m - wst[lo]));
+  };
+  if (win_sm) {
+    for (int m = tid; m < W; m += BT) {
+      int u;
+      const int j = member(m, u);
+      sid[m] = j;
+      skey[m] = a.ids ? __ldg(a.ids + j) : j;
+#pragma unroll
+      for (int k = 0; k < D; ++k) scrd[k * E::WCAP + m] = Prec<P>::cvt(__ldg(e.x[k] + j));
+    }
+  }
+  auto key_of = [&](int m) -> int {
+    if (win_sm) return skey[m];
+    int u;
+    const int j = member(m, u);
+    return a.ids ? __ldg(a.ids + j) : j;
+  };
+  auto id_of = [&](int m) -> int {
+    int u;
+    return win_sm ? sid[m] : member(m, u);
+  };
+  auto crd_of = [&](int m, int k) -> T {
+    if (win_sm) return scrd[k * E::WCAP + m];
+    int u;
+    return Prec<P>::cvt(__ldg(e.x[k] + member(m, u)));
+  };
+
+  // runs: chunk ranges (tri) and the CTA's chunk span
+  if (tid < x1 - x0) {
+    const int t = x0 + tid, u = t - x0 + 2;
+    const int len = (wst[u + 2] - wst[u - 1]);
+    const int64_t slot = rslot[tid];
+    const int nch = (len + 3) >> 2;
+    a.tri[crow + t] = make_int2((int)(slot >> 2), (int)((slot >> 2) + nch));
+    if (tid == 0) s_ch0 = slot >> 2;
+    if (t == x1 - 1) s_nch = (int)((slot >> 2) + nch - (rslot[0] >> 2));
+  }
+  __syncthreads();
+  const int64_t ch0 = s_ch0;
+  const int nch = s_nch;
+  const bool out_sm = nch <= E::OCAP;
+
+  T nanv;
+  if constexpr (P == FP16) nanv = hbits(0x7E00u); else nanv = T(NAN);
+  // sentinel fill of the CTA's chunks (records past each run's end stay sentinels)
+  if (out_sm) {
+    for (int q = tid; q < nch * 4; q += BT) {
+      const int c = q >> 2, l = q & 3;
+#pragma unroll
+      for (int k = 0; k < D; ++k) *rec_el<D, P, MODE>(sch, c, k, l) = nanv;
+      if constexpr (MODE == MODE_RCLL) *rec_el<D, P, MODE>(sch, c, D, l) = T(0.0f);
+      stag[q] = 0xFFFFFFFFu;
+    }
+  } else {
+    // direct: pad records of each run
+    for (int t = x0 + tid; t < x1; t += BT) {
+      const int u = t - x0 + 2;
+      const int len = wst[u + 2] - wst[u - 1];
+      const int64_t slot = rslot[t - x0];
+      for (int q = len; q < ((len + 3) & ~3); ++q) {
+#pragma unroll
+        for (int k = 0; k < D; ++k) store_el<D, P, MODE>(a.qc, slot + q, k, nanv);
+        if constexpr (MODE == MODE_RCLL) store_el<D, P, MODE>(a.qc, slot + q, D, T(0.0f));
+        reinterpret_cast<unsigned*>(a.qtag)[slot + q] = 0xFFFFFFFFu;
+      }
+    }
+  }
+  __syncthreads();
+
+  // number of keys < key in window cell u
+  auto less_in = [&](int u, int key) {
+    int lo = wst[u], hi = wst[u + 1];
+    if (win_sm && hi - lo <= 16) {
+      int c = 0;
+      for (int q = lo; q < hi; ++q) c += skey[q] < key;
+      return c;
+    }
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (key_of(mid) < key) lo = mid + 1; else hi = mid;
+    }
+    return lo - wst[u];
+  };
+
+  // records: members of window cells 1 .. XB+2 (x0-1 .. x1)
+  const int mlo = wst[1], mhi = wst[min(x1 - x0 + 3, NW)];
+  for (int m = mlo + tid; m < mhi; m += BT) {
+    int u = 1, hi = NW;  // last u with wst[u] <= m
+    while (hi - u > 1) {
+      const int mid = (u + hi) >> 1;
+      if (wst[mid] <= m) u = mid; else hi = mid;
+    }
+    const int idx = m - wst[u];
+    const int key = key_of(m), j = id_of(m);
+    T c[3];
+#pragma unroll
+    for (int k = 0; k < D; ++k) c[k] = crd_of(m, k);
+    // runs centred at local u-1, u, u+1 owned by this CTA (local 2 .. x1-x0+1)
+    int lt[3];
+    lt[0] = u > 1 ? less_in(u - 2, key) : 0;
+    lt[1] = less_in(u - 1, key);
+    lt[2] = u + 1 < NW ? less_in(u + 1, key) : 0;
+    const int lt3 = u + 2 < NW ? less_in(u + 2, key) : 0;
+#pragma unroll
+    for (int Lr = 0; Lr < 3; ++Lr) {  // member is list Lr of the run centred at local v
+      const int v = u + 1 - Lr;
+      if (v < 2 || v >= x1 - x0 + 2) continue;
+      // other lists of run v: cells v-1, v, v+1 except u
+      int pos = idx;
+      if (Lr == 0) pos += lt[2] + lt3;              // cells u+1, u+2
+      else if (Lr == 1) pos += lt[1] + lt[2];       // cells u-1, u+1
+      else pos += lt[0] + lt[1];                    // cells u-2, u-1
+      const int t = x0 + v - 2;
+      const int64_t rec = rslot[v - 2] + pos;
+      T cx = c[0];
+      if constexpr (MODE == MODE_CLL) {
+        const int raw = wraw[u];
+        const int w = raw < 0 ? -1 : (raw >= nx ? 1 : 0);
+        if (w != 0) {  // round_to(prec, x + shift), nnps.cpp:116
+          T sh;
+          if constexpr (P == FP16) sh = hbits(e.pc.h_sh[0]);
+          else if constexpr (P == FP32) sh = e.pc.f_sh[0];
+          else sh = e.pc.d_sh[0];
+          if constexpr (P == FP16) cx = __hadd_rn(cx, w > 0 ? sh : __hneg(sh));
+          else cx = f_add(cx, w > 0 ? sh : -sh);
+        }
+      }
+      const uint32_t tag = a.ids ? (uint32_t)key : (uint32_t)j;
+      if (out_sm) {
+        const int lr = (int)(rec - 4 * ch0);
+        *rec_el<D, P, MODE>(sch, lr >> 2, 0, lr & 3) = cx;
+#pragma unroll
+        for (int k = 1; k < D; ++k) *rec_el<D, P, MODE>(sch, lr >> 2, k, lr & 3) = c[k];
+        if constexpr (MODE == MODE_RCLL) *rec_el<D, P, MODE>(sch, lr >> 2, D, lr & 3) = (T)(float)(1 - Lr);
+        stag[lr] = tag;
+      } else {
+        store_el<D, P, MODE>(a.qc, rec, 0, cx);
+#pragma unroll
+        for (int k = 1; k < D; ++k) store_el<D, P, MODE>(a.qc, rec, k, c[k]);
+        if constexpr (MODE == MODE_RCLL) store_el<D, P, MODE>(a.qc, rec, D, (T)(float)(1 - Lr));
+        reinterpret_cast<uint32_t*>(a.qtag)[rec] = tag;
+      }
+      if (Lr == 1) {  // own cell: pos_own and the self record
+        a.selfpos[j] = (int)rec;
+        T own[3] = {c[0], D > 1 ? c[1] : T(0.0f), D > 2 ? c[2] : T(0.0f)};
+        typename Coord<D, P>::T pk;
+        if constexpr (P == FP16) {
+          const __half2 xy = __halves2half2(own[0], D > 1 ? own[1] : hbits(0));
+          if constexpr (D == 3) pk = make_uint2(h2u(xy), h2u(__halves2half2(own[2], hbits(0))));
+          else pk = xy;
+        } else if constexpr (D == 1) {
+          pk = own[0];
+        } else if constexpr (D == 2) {
+          pk.x = own[0];
+          pk.y = own[1];
+        } else {
+          pk.x = own[0];
+          pk.y = own[1];
+          pk.z = own[2];
+          pk.w = T(0);
+        }
+        reinterpret_cast<typename Coord<D, P>::T*>(const_cast<void*>(a.pos_own))[j] = pk;
+      }
+    }
+  }
+  __syncthreads();
+  if (out_sm) {  // stream the CTA's chunks and id quads
+    const uint4* src = reinterpret_cast<const uint4*>(sch);
+    uint4* dst = reinterpret_cast<uint4*>(static_cast<char*>(a.qc) + ch0 * L::BYTES);
+    if constexpr (L::BYTES >= 16) {
+      for (int q = tid; q < nch * (L::BYTES / 16); q += BT) dst[q] = src[q];
+    } else {
+      const uint2* s2 = reinterpret_cast<const uint2*>(sch);
+      uint2* d2 = reinterpret_cast<uint2*>(static_cast<char*>(a.qc) + ch0 * L::BYTES);
+      for (int q = tid; q < nch; q += BT) d2[q] = s2[q];
+    }
+    const uint4* ts = reinterpret_cast<const uint4*>(stag);
+    uint4* td = reinterpret_cast<uint4*>(a.qtag) + ch0;
+    for (int q = tid; q < nch; q += BT) td[q] = ts[q];
+  }
+}
+
 template <int D, int P, int M>
-static void encode_cells(int n, int64_t C, int nx, int wrapx, const PrecConsts& pc,
-                         const double* const x[3], const int32_t* items, const int32_t* start,
-                         void* pos_csr, int32_t* cell_slot, const SweepArgs& a, cudaStream_t st) {
-  k_encode_own<D, P, M><<<(n + 255) / 256, 256, 0, st>>>(n, x[0], x[1], x[2], items, pos_csr,
-                                                         cell_slot, a);
-  k_encode_runs<D, P, M><<<(unsigned)((C + 255) / 256), 256, 0, st>>>(C, nx, wrapx, start, a);
-  k_encode_members<D, P, M><<<(n + 255) / 256, 256, 0, st>>>(n, nx, wrapx, pc, start, items,
-                                                             cell_slot, pos_csr, a);
+static int encode_cells(int n, int64_t C, int nx, int wrapx, const PrecConsts& pc,
+                        const double* const x[3], const int32_t* items, const int32_t* start,
+                        void* pos_csr, int32_t* cell_slot, const SweepArgs& a, cudaStream_t st) {
+  (void)n;
+  (void)pos_csr;
+  (void)cell_slot;
+  using E = EncShape<D, P>;
+  EncArgs e;
+  e.nx = nx;
+  e.nxb = (nx + E::XB - 1) / E::XB;
+  e.wrapx = wrapx;
+  e.nrows = C / nx;
+  e.start = start;
+  e.items = items;
+  for (int k = 0; k < 3; ++k) e.x[k] = x[k];
+  e.pc = pc;
+  constexpr size_t smem = enc_smem_bytes<D, P, M>();
+  cudaFuncSetAttribute(k_encode_rows<D, P, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  k_encode_rows<D, P, M><<<(unsigned)(e.nrows * e.nxb), E::BT, smem, st>>>(e, a);
+  return 1;
 }
 
 template <int D, int P>
@@ -1245,10 +1591,8 @@ static int encode_t(int mode, int n, int64_t C, int nx, int wrapx, const PrecCon
   }
   if (C == 0) return 0;
   if (mode == MODE_RCLL)
-    encode_cells<D, P, MODE_RCLL>(n, C, nx, wrapx, pc, x, items, start, pos_csr, cell_slot, a, st);
-  else
-    encode_cells<D, P, MODE_CLL>(n, C, nx, wrapx, pc, x, items, start, pos_csr, cell_slot, a, st);
-  return 3;
+    return encode_cells<D, P, MODE_RCLL>(n, C, nx, wrapx, pc, x, items, start, pos_csr, cell_slot, a, st);
+  return encode_cells<D, P, MODE_CLL>(n, C, nx, wrapx, pc, x, items, start, pos_csr, cell_slot, a, st);
 }
 
 // Returns the number of kernel launches issued (n > 0).
@@ -1264,14 +1608,20 @@ int launch_encode(int dim, int prec, int mode, int n, int64_t C, int nx, int wra
   return 0;
 }
 
+// Returns the number of tile tickets the launch consumes (one per block, or one
+// per warp for k_rcll16); the caller advances its ticket base by exactly that.
 template <int D, int P, int M>
-static void sweep_t(const SweepArgs& a, cudaStream_t st) {
+static int64_t sweep_t(const SweepArgs& a, cudaStream_t st) {
   using S = Shape<D>;
-  const unsigned nb = (unsigned)((a.nrows + S::BT - 1) / S::BT);
-  if constexpr (P == FP16 && M == MODE_RCLL && D >= 2)
-    k_rcll16<D, S::BT, S::PCAP, S::WMAX><<<nb, S::BT, 0, st>>>(a);
-  else
-    k_sweep<D, P, M, S::BT, S::PCAP, S::WMAX><<<nb, S::BT, 0, st>>>(a);
+  if constexpr (P == FP16 && M == MODE_RCLL && D >= 2) {
+    const int64_t nb = (a.nrows + S::BT - 1) / S::BT;
+    k_rcll16<D, S::BT, S::PCAP, S::WMAX><<<(unsigned)nb, S::BT, 0, st>>>(a);
+    return nb;
+  } else {
+    const int64_t nb = (a.nrows + S::BT - 1) / S::BT;
+    k_sweep<D, P, M, S::BT, S::PCAP, S::WMAX><<<(unsigned)nb, S::BT, 0, st>>>(a);
+    return nb;
+  }
 }
 
 #define SW(FN, D, P, M) \
@@ -1282,8 +1632,11 @@ static void sweep_t(const SweepArgs& a, cudaStream_t st) {
   SWP(FN, 1, MODE_CLL) SWP(FN, 2, MODE_CLL) SWP(FN, 3, MODE_CLL)    \
   SWP(FN, 1, MODE_ALL) SWP(FN, 2, MODE_ALL) SWP(FN, 3, MODE_ALL)
 
-// The single-pass sweep: offsets[0..nrows] and the rows.
-void launch_sweep(int dim, int prec, int mode, const SweepArgs& a, cudaStream_t st) { SWA(sweep_t) }
+// The single-pass sweep: offsets[0..nrows] and the rows. Returns the tickets used.
+int64_t launch_sweep(int dim, int prec, int mode, const SweepArgs& a, cudaStream_t st) {
+  SWA(sweep_t)
+  return 0;
+}
 
 #undef SWA
 #undef SWP

@@ -1,13 +1,13 @@
 #!/bin/bash
 # Quick GPU iteration (under gpurun): C2 and C3 bench lines and one ncu --set full
-# capture of k_sweep.   tools/quick.sh <tag> [--tests] [--no-ncu]
+# capture of the sweep kernel.   tools/quick.sh <tag> [--tests] [--no-ncu]
 TAG=$1; shift
 mkdir -p gpurun_out
 for a in "$@"; do
-  [ "$a" = "--tests" ] && { timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_${TAG}.log 2>&1; tail -3 gpurun_out/pytest_${TAG}.log; }
+  [ "$a" = "--tests" ] && { timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_${TAG}.log 2>&1; tail -3 gpurun_out/pytest_${TAG}.log; }
 done
 for C in C2 C3; do
-  python bench.py --config $C --no-cpu-baseline --e2e-steps 2 > gpurun_out/bench_${TAG}_${C}.json 2> gpurun_out/bench_${TAG}_${C}.err
+  timeout 300 python bench.py --config $C --no-cpu-baseline --e2e-steps 2 > gpurun_out/bench_${TAG}_${C}.json 2> gpurun_out/bench_${TAG}_${C}.err
   python - "$TAG" "$C" <<'PY'
 import json, sys
 t, c = sys.argv[1], sys.argv[2]
@@ -20,7 +20,7 @@ except Exception as e:
 PY
 done
 case " $* " in *" --no-ncu "*) exit 0;; esac
-ncu --set full --clock-control none --import-source on -k regex:"k_(sweep|rcll16)" -s 4 -c 1 \
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:"k_(sweep|rcll16)" -s 4 -c 1 \
     -o gpurun_out/prof_${TAG} python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 \
     > gpurun_out/ncu_${TAG}.log 2>&1
 tail -1 gpurun_out/ncu_${TAG}.log
