@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libsphx_cuda.so")
+LIB_PATH = os.environ.get("SPHX_CUDA_LIB") or os.path.join(PKG, "lib", "libsphx_cuda.so")
 
 FP64, FP32, FP16 = 0, 1, 2
 PRECISIONS = {"fp64": FP64, "fp32": FP32, "fp16": FP16}

@@ -324,6 +324,7 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
   a.c = make_consts(mode, prec, g, h);
   a.tri = ctx->tri.as<int2>();
   a.qc = ctx->qc.p;
+  a.nchunks = chunks;
   a.qtag = ctx->qtag.p;
   a.selfpos = ctx->selfpos.as<int32_t>();
   a.pos_own = ctx->pos_own.p;

@@ -41,6 +41,7 @@ struct SweepArgs {
   void* qc;                   // [chunks] records: coordinate quads per axis (x pre-shifted
                               // for CLL), then the RCLL x offset quad dc = cx_i - cx_j
   void* qtag;                 // [chunks] uint4 particle ids (~0 = sentinel)
+  int64_t nchunks;            // chunks allocated for qc / qtag
   int32_t* selfpos;           // [n] record index of particle i in its own-cell run
   const void* pos_own;        // packed coords in particle order
   const int32_t* cellk[3];    // RCLL: RelCoords::cell[k] (particle order)
