@@ -764,8 +764,16 @@ __device__ __forceinline__ void prefetch_l1(const void* p) {
 
 // Tiles of BT consecutive rows (one block each): A (hit words) -> block scan ->
 // publish -> B (sorted rows into the packed tile) -> resolve -> offsets, stream.
+template <int D>
+struct R16Shape {
+  static constexpr int BT = D == 3 ? 64 : 128;
+  static constexpr int PCAP = D == 3 ? 64 * 60 : 128 * 20;  // packed rows per tile
+  static constexpr int WMAX = D == 3 ? 20 : 4;              // hit words kept per row
+  static constexpr int MINB = D == 3 ? 14 : 12;             // CTAs per SM (register budget)
+};
+
 template <int D, int BT, int PCAP, int WMAX>
-__global__ void __launch_bounds__(BT, D == 3 ? 12 : 8) k_rcll16(SweepArgs a) {
+__global__ void __launch_bounds__(BT, R16Shape<D>::MINB) k_rcll16(SweepArgs a) {
   constexpr int NR = R16<D>::NR;
   __shared__ __align__(16) int32_t PK[PCAP + 4];
   __shared__ unsigned NIB[WMAX * BT];
@@ -1237,6 +1245,7 @@ struct Shape {
 // Host-side launchers (called from capi.cu)
 // ------------------------------------------------------------------------------
 int sweep_tile(int dim, int prec, int mode) {
+  if (prec == FP16 && mode == MODE_RCLL && dim >= 2) return dim == 3 ? R16Shape<3>::BT : R16Shape<2>::BT;
   return dim == 3 ? Shape<3>::BT : Shape<2>::BT;
 }
 size_t coord_bytes(int dim, int prec) {
@@ -1614,8 +1623,9 @@ template <int D, int P, int M>
 static int64_t sweep_t(const SweepArgs& a, cudaStream_t st) {
   using S = Shape<D>;
   if constexpr (P == FP16 && M == MODE_RCLL && D >= 2) {
-    const int64_t nb = (a.nrows + S::BT - 1) / S::BT;
-    k_rcll16<D, S::BT, S::PCAP, S::WMAX><<<(unsigned)nb, S::BT, 0, st>>>(a);
+    using R = R16Shape<D>;
+    const int64_t nb = (a.nrows + R::BT - 1) / R::BT;
+    k_rcll16<D, R::BT, R::PCAP, R::WMAX><<<(unsigned)nb, R::BT, 0, st>>>(a);
     return nb;
   } else {
     const int64_t nb = (a.nrows + S::BT - 1) / S::BT;
