@@ -26,6 +26,7 @@ size_t coord_bytes(int dim, int prec);
 size_t chunk_bytes(int dim, int prec, int mode);
 int64_t chunk_capacity(int mode, int64_t n, int64_t C);
 int sweep_tile(int dim, int prec, int mode);
+int hit_words(int dim, int prec, int mode);
 // binning.cu
 int64_t scan_tiles(int64_t C);
 void launch_locate(int mode, const LocateArgs& a, cudaStream_t st);
@@ -118,7 +119,7 @@ struct sphx_context {
   // encode / sweep scratch
   Buf pos_own, pos_csr, cell_slot, tri, qc, qtag, selfpos;
   // single-pass sweep: look-back words (epoch-tagged) and the tile ticket
-  Buf sw_tiles, sw_ticket;
+  Buf sw_tiles, sw_ticket, sw_rowk, sw_hitw;
   unsigned long long sw_tick = 0;
   unsigned sw_epoch = 0;
   int64_t sw_ntiles = 0;
@@ -359,6 +360,13 @@ int run_sweep(sphx_context* ctx, int dim, int prec, int mode, SweepArgs& a, int3
     CK(cudaMemsetAsync(ctx->sw_ticket.p, 0, sizeof(unsigned long long), st));
     ctx->sw_tick = 0;
   }
+  const int hw = hit_words(dim, prec, mode);
+  if (hw > 0) {
+    TRY(ctx->sw_rowk.ensure(sizeof(int32_t) * (size_t)a.nrows));
+    TRY(ctx->sw_hitw.ensure(sizeof(unsigned) * (size_t)hw * (size_t)a.nrows));
+    a.rowk = ctx->sw_rowk.as<int32_t>();
+    a.hitw = ctx->sw_hitw.as<unsigned>();
+  }
   a.items = d_items;
   a.capacity = capacity;
   a.tiles = ctx->sw_tiles.as<unsigned long long>();
@@ -368,7 +376,7 @@ int run_sweep(sphx_context* ctx, int dim, int prec, int mode, SweepArgs& a, int3
   const int64_t used = launch_sweep(dim, prec, mode, a, st);
   CKL();
   ctx->sw_tick += (unsigned long long)used;
-  ++ctx->launches;
+  ctx->launches += hw > 0 ? 2 : 1;  // test + emit kernels, or the single-pass sweep
   if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], st));
   return SPHX_OK;
 }
@@ -549,7 +557,7 @@ void sphx_destroy(sphx_context* ctx) {
   Buf* all[] = {&ctx->in_x[0], &ctx->in_x[1], &ctx->in_x[2], &ctx->in_cell[0], &ctx->in_cell[1],
                 &ctx->in_cell[2], &ctx->in_items, &ctx->in_start, &ctx->in_cellof, &ctx->pos_own,
                 &ctx->tri, &ctx->pos_csr, &ctx->cell_slot, &ctx->qc,
-                &ctx->qtag, &ctx->selfpos, &ctx->sw_tiles, &ctx->sw_ticket, &ctx->t_offsets, &ctx->t_items,
+                &ctx->qtag, &ctx->selfpos, &ctx->sw_tiles, &ctx->sw_ticket, &ctx->sw_rowk, &ctx->sw_hitw, &ctx->t_offsets, &ctx->t_items,
                 &ctx->b_counts, &ctx->b_slot, &ctx->b_bad, &ctx->b_tiles, &ctx->b_out_cellof,
                 &ctx->b_out_start, &ctx->b_out_items, &ctx->b_rel[0], &ctx->b_rel[1],
                 &ctx->b_rel[2], &ctx->b_cell[0], &ctx->b_cell[1], &ctx->b_cell[2]};

@@ -55,6 +55,8 @@ struct SweepArgs {
   unsigned long long* ticket; // tile ticket counter (monotone across calls)
   unsigned long long tick0;   // ticket value at this call's first tile
   unsigned epoch;             // this call's look-back epoch (1..65535)
+  int32_t* rowk;              // [nrows] row lengths of the test pass (bit 31: words overflowed)
+  unsigned* hitw;             // [W][nrows] hit words of the test pass
 };
 
 // Look-back words carry flag and value in one 64-bit word, so relaxed gpu-scope

@@ -31,6 +31,7 @@
 // keep subnormals, and sqrt(acc) < cutoff is the exact monotone test acc < thr.
 
 #include <climits>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -922,6 +923,198 @@ __global__ void __launch_bounds__(BT, R16Shape<D>::MINB) k_rcll16(SweepArgs a) {
   stream_tile<BT>(gout, SharedRow{(uint32_t)__cvta_generic_to_shared(PK)}, btot, tid);
 }
 
+// ------------------------------------------------------------------------------
+// FP16 RCLL in two kernels. The candidate tests are latency-bound and want every
+// resident warp they can get, while the ordered part (scan, look-back, sorted rows,
+// coalesced stores) is light; splitting them keeps the look-back off the tests.
+//   k_r16_test: one thread per row, no shared memory, no inter-block dependency:
+//     hit words (groups of <= 8 chunks of a run, in (dz, dy) run order) -> hitw,
+//     row length -> rowk (bit 31: more than W words).
+//   k_r16_emit: tiles of BT rows: block scan of rowk, look-back, sorted rows into a
+//     packed shared tile from the hit words and the id quads, 16-byte stores.
+// ------------------------------------------------------------------------------
+template <int D>
+struct R16Two {
+  static constexpr int W = D == 3 ? 16 : 4;          // hit words per row
+  static constexpr int TB = 256, TMINB = D == 3 ? 3 : 5;   // test kernel: threads, CTAs/SM
+  static constexpr int BT = D == 3 ? 64 : 128;       // emit kernel tile
+  static constexpr int PCAP = D == 3 ? 64 * 60 : 128 * 20;
+  static constexpr int EMINB = D == 3 ? 12 : 10;
+};
+
+// the row's run in each (dz, dy) slot q (empty: cb == ce), RCLL cell of particle i
+template <int D>
+__device__ __forceinline__ void r16_runs(const SweepArgs& a, int i, bool valid, int (&cb)[R16<D>::NR],
+                                         int (&ce)[R16<D>::NR]) {
+  constexpr int NR = R16<D>::NR;
+  const int nx = a.g.counts[0], ny = a.g.counts[1], nz = a.g.counts[2];
+  const int cx = __ldg(a.cellk[0] + i), cy = __ldg(a.cellk[1] + i);
+  const int cz = D == 3 ? __ldg(a.cellk[2] + i) : 0;
+  const bool ok = valid && cx >= 0 && cx < nx && cy >= 0 && cy < ny && cz >= 0 && cz < nz;
+#pragma unroll
+  for (int q = 0; q < NR; ++q) {
+    const int dy = (q % 3) - 1, dz = D == 3 ? (q / 3) - 1 : 0;
+    int y = cy + dy, z = cz + dz;
+    bool in = ok;
+    if (y < 0) { y += ny; in = in && a.g.wrap[1]; }
+    else if (y >= ny) { y -= ny; in = in && a.g.wrap[1]; }
+    if (D == 3) {
+      if (z < 0) { z += nz; in = in && a.g.wrap[2]; }
+      else if (z >= nz) { z -= nz; in = in && a.g.wrap[2]; }
+    }
+    int2 t = make_int2(0, 0);
+    if (in) t = __ldg(a.tri + ((int64_t)z * ny + y) * nx + cx);
+    cb[q] = t.x;
+    ce[q] = t.y;
+  }
+}
+
+// everything the tests of one particle need
+template <int D>
+struct R16Own {
+  __half2 r2[3], hh2[3], hc2, thr2;
+  unsigned hcy, hcz;
+  int selfch;
+  unsigned selfmask;
+  __device__ __forceinline__ void init(const SweepArgs& a, int i) {
+    const typename Coord<D, FP16>::T o = ldg<typename Coord<D, FP16>::T>(a.pos_own, i);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      r2[k] = k < D ? __half2half2(axis_of<D, FP16>(o, k)) : u2h(0u);
+      hh2[k] = __half2half2(hbits(a.c.h_hh[k]));
+    }
+    hc2 = __half2half2(hbits(a.c.h_cc[0]));
+    thr2 = __half2half2(hbits(a.c.h_thr));
+    hcy = a.c.h_cc[1];
+    hcz = a.c.h_cc[2];
+    const int self = __ldg(a.selfpos + i);
+    selfch = self >> 2;
+    selfmask = ~(1u << (28 + (self & 3)));
+  }
+  // hit word of chunks [g, e) of the run in slot q
+  template <int Q>
+  __device__ __forceinline__ unsigned group(const char* __restrict__ qc, int g, int e) const {
+    constexpr int dy = (Q % 3) - 1, dz = D == 3 ? (Q / 3) - 1 : 0;
+    const __half2 ccy = cc_of(hcy, dy), ccz = cc_of(hcz, dz);
+    unsigned acc = 0;
+#pragma unroll 4
+    for (int ch = g; ch < e; ++ch) {
+      r16_chunk<D>(qc, ch, r2, hh2, hc2, thr2, ccy, ccz, acc);
+      if (Q == R16<D>::NR / 2 && ch == selfch) acc &= selfmask;
+    }
+    return acc >> (4 * (8 - (e - g)));
+  }
+};
+
+template <int D, int Q, class F>
+__device__ __forceinline__ void r16_for_slots(F&& f) {
+  if constexpr (Q < R16<D>::NR) {
+    f(std::integral_constant<int, Q>());
+    r16_for_slots<D, Q + 1>(f);
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(R16Two<D>::TB, R16Two<D>::TMINB) k_r16_test(SweepArgs a) {
+  constexpr int NR = R16<D>::NR, W = R16Two<D>::W;
+  const int r = blockIdx.x * R16Two<D>::TB + threadIdx.x;
+  if (r >= a.nrows) return;
+  const int i = a.row0 + r;
+  const char* __restrict__ qc = static_cast<const char*>(a.qc);
+  R16Own<D> own;
+  own.init(a, i);
+  int cb[NR], ce[NR];
+  r16_runs<D>(a, i, true, cb, ce);
+  int k = 0, w = 0;
+  r16_for_slots<D, 0>([&](auto qv) {
+    constexpr int Q = decltype(qv)::value;
+    for (int g = cb[Q]; g < ce[Q]; g += 8) {
+      const unsigned word = own.template group<Q>(qc, g, min(g + 8, ce[Q]));
+      k += __popc(word);
+      if (w < W) a.hitw[(int64_t)w * a.nrows + r] = word;
+      ++w;
+    }
+  });
+  a.rowk[r] = (int)((unsigned)k | (w > W ? 0x80000000u : 0u));
+}
+
+template <int D, int BT, int PCAP>
+__global__ void __launch_bounds__(BT, R16Two<D>::EMINB) k_r16_emit(SweepArgs a) {
+  constexpr int NR = R16<D>::NR, W = R16Two<D>::W;
+  __shared__ __align__(16) int32_t PK[PCAP + 4];
+  __shared__ int s_w[BT / 32];
+  __shared__ int s_tile;
+  __shared__ long long s_base;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = (int)(atomicAdd(a.ticket, 1ull) - a.tick0);
+  __syncthreads();
+  const int tile = s_tile;
+  const int r = tile * BT + tid;
+  const bool valid = r < a.nrows;
+  const int i = a.row0 + (valid ? r : 0);
+  const unsigned kw = valid ? (unsigned)__ldg(a.rowk + r) : 0u;
+  const int k = (int)(kw & 0x7FFFFFFFu);
+  const bool ovf = kw >> 31;
+
+  const int incl = warp_inclusive_scan(k);
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  int wbase = 0, btot = 0;
+#pragma unroll
+  for (int u = 0; u < BT / 32; ++u) {
+    wbase += u < warp ? s_w[u] : 0;
+    btot += s_w[u];
+  }
+  const int excl = wbase + incl - k;
+  if (tid == 0) lookback_publish(a.tiles, tile, btot, a.epoch);
+
+  const char* __restrict__ qc = static_cast<const char*>(a.qc);
+  const uint4* __restrict__ tags = reinterpret_cast<const uint4*>(a.qtag);
+  // the sorted row: runs in (dz, dy) order, hits appended with predicated stores;
+  // a run whose first id is below the row's last is merged in (runs interleave
+  // only where two cell rows / planes share id ranges)
+  auto build = [&](const auto& dst) {
+    int cb[NR], ce[NR];
+    r16_runs<D>(a, i, true, cb, ce);
+    R16Own<D> own;
+    if (ovf) own.init(a, i);
+    int kk = 0, w = 0;
+    r16_for_slots<D, 0>([&](auto qv) {
+      constexpr int Q = decltype(qv)::value;
+      const int gs = kk;
+      for (int g = cb[Q]; g < ce[Q]; g += 8) {
+        unsigned word = w < W ? __ldg(a.hitw + (int64_t)w * a.nrows + r)
+                              : own.template group<Q>(qc, g, min(g + 8, ce[Q]));
+        ++w;
+        for (int ch = g; word; ++ch, word >>= 4) {
+          const unsigned m = word & 15u;
+          if (m) append4(dst, kk, m, __ldg(tags + ch));
+        }
+      }
+      if (gs > 0 && kk > gs && dst.ld(gs) < dst.ld(gs - 1)) merge_tail(dst, gs, kk);
+    });
+  };
+  const bool fits = btot <= PCAP;
+  if (fits && valid && k > 0)
+    build(SharedRow{(uint32_t)__cvta_generic_to_shared(PK) + 4u * (uint32_t)excl});
+
+  if (warp == 0) {
+    const long long b = lookback_resolve(a.tiles, tile, btot, a.epoch);
+    if (lane == 0) s_base = b;
+  }
+  __syncthreads();
+  const long long base = s_base;
+  if (valid) a.offsets[r] = base + excl;
+  if (r == a.nrows - 1) a.offsets[a.nrows] = base + excl + k;
+  if (base + btot > a.capacity) return;
+  int32_t* gout = a.items + base;
+  if (!fits) {
+    if (valid && k > 0) build(GlobalRow{gout + excl});
+    return;
+  }
+  stream_tile<BT>(gout, SharedRow{(uint32_t)__cvta_generic_to_shared(PK)}, btot, tid);
+}
+
 // The whole table in one pass over tiles of BT consecutive rows (particle order).
 //   A. each thread tests its particle's candidates; the hit words go to shared
 //      memory (WMAX per thread; later groups are re-tested in B) and the row
@@ -1245,13 +1438,18 @@ struct Shape {
 // Host-side launchers (called from capi.cu)
 // ------------------------------------------------------------------------------
 int sweep_tile(int dim, int prec, int mode) {
-  if (prec == FP16 && mode == MODE_RCLL && dim >= 2) return dim == 3 ? R16Shape<3>::BT : R16Shape<2>::BT;
+  if (prec == FP16 && mode == MODE_RCLL && dim >= 2) return dim == 3 ? R16Two<3>::BT : R16Shape<2>::BT;
   return dim == 3 ? Shape<3>::BT : Shape<2>::BT;
 }
 size_t coord_bytes(int dim, int prec) {
   if (prec == FP16) return dim == 3 ? 8 : 4;
   if (prec == FP32) return dim == 1 ? 4 : (dim == 2 ? 8 : 16);
   return dim == 1 ? 8 : (dim == 2 ? 16 : 32);
+}
+// hit words per row the two-kernel FP16 RCLL sweep keeps (0: single kernel)
+int hit_words(int dim, int prec, int mode) {
+  if (prec == FP16 && mode == MODE_RCLL && dim == 3) return R16Two<3>::W;
+  return 0;
 }
 size_t chunk_bytes(int dim, int prec, int mode) {
 #define CB(D, P, M) if (dim == D && prec == P && mode == M) return ChunkLay<D, P, M>::BYTES;
@@ -1622,7 +1820,15 @@ int launch_encode(int dim, int prec, int mode, int n, int64_t C, int nx, int wra
 template <int D, int P, int M>
 static int64_t sweep_t(const SweepArgs& a, cudaStream_t st) {
   using S = Shape<D>;
-  if constexpr (P == FP16 && M == MODE_RCLL && D >= 2) {
+  if constexpr (P == FP16 && M == MODE_RCLL && D == 3) {
+    // 3-D: tests and ordered emission in separate kernels (R16Two)
+    using R = R16Two<D>;
+    k_r16_test<D><<<(unsigned)((a.nrows + R::TB - 1) / R::TB), R::TB, 0, st>>>(a);
+    const int64_t nb = (a.nrows + R::BT - 1) / R::BT;
+    k_r16_emit<D, R::BT, R::PCAP><<<(unsigned)nb, R::BT, 0, st>>>(a);
+    return nb;
+  } else if constexpr (P == FP16 && M == MODE_RCLL && D == 2) {
+    // 2-D: one fused kernel (the look-back wait hides the emission)
     using R = R16Shape<D>;
     const int64_t nb = (a.nrows + R::BT - 1) / R::BT;
     k_rcll16<D, R::BT, R::PCAP, R::WMAX><<<(unsigned)nb, R::BT, 0, st>>>(a);
