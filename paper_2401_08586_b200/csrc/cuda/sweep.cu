@@ -936,7 +936,7 @@ __global__ void __launch_bounds__(BT, R16Shape<D>::MINB) k_rcll16(SweepArgs a) {
 template <int D>
 struct R16Two {
   static constexpr int W = D == 3 ? 16 : 4;          // hit words per row
-  static constexpr int TB = 256, TMINB = D == 3 ? 3 : 5;   // test kernel: threads, CTAs/SM
+  static constexpr int TB = 256, TMINB = D == 3 ? 4 : 5;   // test kernel: threads, CTAs/SM
   static constexpr int BT = D == 3 ? 64 : 128;       // emit kernel tile
   static constexpr int PCAP = D == 3 ? 64 * 60 : 128 * 20;
   static constexpr int EMINB = D == 3 ? 12 : 10;
