@@ -20,6 +20,10 @@
  *   sphx_rebuild_members <- void CellGrid::rebuild_members(const RelCoords&)
  *                                                                   cell_grid.hpp:150, cell_grid.cpp:86-108
  *   sphx_table_copy      <- (ownership hand-off of the returned NeighborTable, nnps.hpp:16-26)
+ *   sphx_table_distances / sphx_rcll_distances_device
+ *                        <- double rel_distance(const RelCoords&, size_t i, size_t j,
+ *                                               const CellGrid&, Precision) for every entry
+ *                                                                   cell_grid.hpp:128, cell_grid.cpp:135-178
  *   sphx_last_error      <- the what() of the exception the reference would throw
  *   (the reference's own C-style template is detail::range_f16_rel_2d & co,
  *    detail/nnps_batch.hpp:13-41)
@@ -190,6 +194,20 @@ int sphx_rcll_rows_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t
                           const int32_t* d_items, const int32_t* d_cell_start, int32_t precision,
                           const int32_t* d_ids, int64_t row0, int64_t nrows, int64_t* d_offsets,
                           int32_t* d_items_out, int64_t capacity);
+
+/* Per-pair distances of an RCLL table (device memory, stream-ordered): d_dist[e]
+ * is the value rcll compared against the cutoff for entry e = (i, items[e]) --
+ * finish(acc) at the precision with the minimum-image cell offset
+ * (nnps.cpp:321-346, 359-362); for pairs that do not wrap a periodic axis it is
+ * exactly rel_distance(rc, i, j, grid, prec) (cell_grid.hpp:128, cell_grid.cpp:135-178). */
+int sphx_rcll_distances_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                               const double* const d_rel[3], const int32_t* const d_cell[3],
+                               int32_t precision, const int64_t* d_offsets,
+                               const int32_t* d_items, double* d_dist);
+/* The same for the table of the last sphx_rcll call on this context (its staged
+ * inputs); dist receives sphx_rcll's *total doubles (host memory, synchronous). */
+int sphx_table_distances(sphx_context* ctx, const sphx_grid_desc* grid, int32_t precision,
+                         double* dist);
 
 /* Un-jittered build_lattice sites with ids [id0, id0 + count) written to d_x
  * (x_k = lo_k + (c_k + 0.5) ds, bit-identical to particle_system.cpp:53). */

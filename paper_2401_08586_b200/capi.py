@@ -92,6 +92,8 @@ def lib():
                                             vp, i64]),
         "sphx_lattice_device": (C.c_int, [vp, i32, C.POINTER(dbl), C.POINTER(dbl), dbl, i64, i64,
                                           p3]),
+        "sphx_rcll_distances_device": (C.c_int, [vp, G, i64, p3, p3, i32, vp, vp, vp]),
+        "sphx_table_distances": (C.c_int, [vp, G, i32, vp]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -108,7 +110,7 @@ EXPORTED = ("sphx_last_error", "sphx_grid_init", "sphx_create", "sphx_destroy",
             "sphx_build_rel_coords_device", "sphx_rebin_device", "sphx_enable_timing",
             "sphx_last_timing", "sphx_build_lattice", "sphx_build_random_uniform",
             "sphx_table_hash", "sphx_build_rel_coords_window_device", "sphx_rcll_rows_device",
-            "sphx_lattice_device")
+            "sphx_lattice_device", "sphx_rcll_distances_device", "sphx_table_distances")
 
 
 def table_hash(offsets: np.ndarray, items: np.ndarray) -> int:
@@ -187,6 +189,8 @@ def _c32(a):
 class Context:
     """One sphx_context: a CUDA stream plus grow-only device buffers."""
 
+    _last_total = 0
+
     def __init__(self, device: int = -1):
         h = C.c_void_p()
         check(lib().sphx_create(device, C.byref(h)))
@@ -247,7 +251,20 @@ class Context:
         tot = C.c_int64()
         check(lib().sphx_rcll(self.h, C.byref(grid), n, _ptr3(rel), _ptr3(cell), len(items),
                               items.ctypes.data, cell_start.ctypes.data, prec, C.byref(tot)))
+        self._last_total = tot.value
         return self._fetch(n, tot.value)
+
+    def table_distances(self, grid: GridDesc, prec: int) -> np.ndarray:
+        """Per-pair distances of the last rcll() table (rel_distance per entry)."""
+        d = np.empty(max(self._last_total, 1), dtype=np.float64)
+        check(lib().sphx_table_distances(self.h, C.byref(grid), prec, d.ctypes.data))
+        return d[:self._last_total]
+
+    def rcll_distances_device(self, grid, rel, cell, prec, offsets, items, dist):
+        self._bind(offsets)
+        check(lib().sphx_rcll_distances_device(self.h, C.byref(grid), rel[0].numel(), _dptr3(rel),
+                                               _dptr3(cell), prec, offsets.data_ptr(),
+                                               items.data_ptr(), dist.data_ptr()))
 
     def cell_link_list(self, grid: GridDesc, x, h: float, items, cell_start, cell_of, prec: int):
         x = [_c64(a) for a in x]

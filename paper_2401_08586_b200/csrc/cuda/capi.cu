@@ -34,6 +34,10 @@ void launch_scan_counts(const int32_t* in, int32_t* out, int64_t C, unsigned lon
                         int* counter, cudaStream_t st);
 void launch_scatter_sort(int n, int64_t C, const int32_t* cell_of, const int32_t* slot,
                          const int32_t* start, int32_t* items, cudaStream_t st);
+int launch_rcll_distances(int dim, int prec, int64_t nrows, const GridConsts& g,
+                          const PrecConsts& pc, const double hc[3], const double* const rel[3],
+                          const int32_t* const cell[3], const int64_t* off,
+                          const int32_t* items, double* dist, cudaStream_t st);
 void launch_lattice(int dim, const double lo[3], double ds, const int64_t counts[3], int64_t id0,
                     int64_t count, double* const x[3], cudaStream_t st);
 }  // namespace sphx_dev
@@ -124,8 +128,9 @@ struct sphx_context {
   unsigned sw_epoch = 0;
   int64_t sw_ntiles = 0;
   // table of the last host-API call
-  Buf t_offsets, t_items;
+  Buf t_offsets, t_items, t_dist;
   int64_t t_n = -1, t_total = 0, t_capacity = 0;
+  bool t_rcll = false;  // the last host table came from sphx_rcll (inputs still staged)
   // binning scratch
   Buf b_counts, b_slot, b_bad, b_tiles, b_out_cellof, b_out_start, b_out_items, b_rel[3], b_cell[3];
 };
@@ -557,7 +562,7 @@ void sphx_destroy(sphx_context* ctx) {
   Buf* all[] = {&ctx->in_x[0], &ctx->in_x[1], &ctx->in_x[2], &ctx->in_cell[0], &ctx->in_cell[1],
                 &ctx->in_cell[2], &ctx->in_items, &ctx->in_start, &ctx->in_cellof, &ctx->pos_own,
                 &ctx->tri, &ctx->pos_csr, &ctx->cell_slot, &ctx->qc,
-                &ctx->qtag, &ctx->selfpos, &ctx->sw_tiles, &ctx->sw_ticket, &ctx->sw_rowk, &ctx->sw_hitw, &ctx->t_offsets, &ctx->t_items,
+                &ctx->qtag, &ctx->selfpos, &ctx->sw_tiles, &ctx->sw_ticket, &ctx->sw_rowk, &ctx->sw_hitw, &ctx->t_offsets, &ctx->t_items, &ctx->t_dist,
                 &ctx->b_counts, &ctx->b_slot, &ctx->b_bad, &ctx->b_tiles, &ctx->b_out_cellof,
                 &ctx->b_out_start, &ctx->b_out_items, &ctx->b_rel[0], &ctx->b_rel[1],
                 &ctx->b_rel[2], &ctx->b_cell[0], &ctx->b_cell[1], &ctx->b_cell[2]};
@@ -615,8 +620,11 @@ int sphx_rcll(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
   }
   TRY(upload(ctx, ctx->in_items, items, sizeof(int32_t) * n));
   TRY(upload(ctx, ctx->in_start, cell_start, sizeof(int32_t) * (C + 1)));
-  return run_host_table(ctx, MODE_RCLL, *grid, n, d_rel, d_cell, ctx->in_items.as<int32_t>(),
-                        ctx->in_start.as<int32_t>(), nullptr, precision, 0.0, total);
+  const int rc = run_host_table(ctx, MODE_RCLL, *grid, n, d_rel, d_cell,
+                                ctx->in_items.as<int32_t>(), ctx->in_start.as<int32_t>(), nullptr,
+                                precision, 0.0, total);
+  ctx->t_rcll = rc == SPHX_OK;
+  return rc;
 }
 
 int sphx_cell_link_list(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
@@ -637,6 +645,7 @@ int sphx_cell_link_list(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n
   TRY(upload(ctx, ctx->in_items, items, sizeof(int32_t) * n));
   TRY(upload(ctx, ctx->in_start, cell_start, sizeof(int32_t) * (C + 1)));
   TRY(upload(ctx, ctx->in_cellof, cell_of, sizeof(int32_t) * n));
+  ctx->t_rcll = false;
   return run_host_table(ctx, MODE_CLL, *grid, n, d_x, nullptr, ctx->in_items.as<int32_t>(),
                         ctx->in_start.as<int32_t>(), ctx->in_cellof.as<int32_t>(), precision, h,
                         total);
@@ -657,6 +666,7 @@ int sphx_all_list(sphx_context* ctx, int32_t dim, int64_t n, const double* const
     TRY(upload(ctx, ctx->in_x[k], x[k], sizeof(double) * n));
     d_x[k] = ctx->in_x[k].as<double>();
   }
+  ctx->t_rcll = false;
   return run_host_table(ctx, MODE_ALL, g, n, d_x, nullptr, nullptr, nullptr, nullptr, precision,
                         h, total);
 }
@@ -800,6 +810,46 @@ int sphx_rebin_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
 }
 
 // ---------------- multi-GPU slab path ----------------
+
+int sphx_rcll_distances_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                               const double* const d_rel[3], const int32_t* const d_cell[3],
+                               int32_t precision, const int64_t* d_offsets,
+                               const int32_t* d_items, double* d_dist) {
+  TRY(check_ctx(ctx));
+  if (!grid) return fail(SPHX_ERR_INVALID_ARGUMENT, "null grid");
+  TRY(check_prec_dim(precision, grid->dim));
+  const GridConsts gc = grid_consts(*grid);
+  const PrecConsts pc = make_consts(MODE_RCLL, precision, *grid, 0.0);
+  double hc[3] = {0.0, 0.0, 0.0};
+  for (int k = 0; k < grid->dim; ++k) hc[k] = grid->hc[k];
+  ctx->launches += launch_rcll_distances(grid->dim, precision, n, gc, pc, hc, d_rel, d_cell,
+                                         d_offsets, d_items, d_dist, ctx->stream);
+  CKL();
+  return SPHX_OK;
+}
+
+int sphx_table_distances(sphx_context* ctx, const sphx_grid_desc* grid, int32_t precision,
+                         double* dist) {
+  TRY(check_ctx(ctx));
+  if (!grid || !dist) return fail(SPHX_ERR_INVALID_ARGUMENT, "null argument");
+  if (ctx->t_n < 0 || !ctx->t_rcll)
+    return fail(SPHX_ERR_INVALID_ARGUMENT, "no rcll table computed on this context");
+  TRY(ctx->t_dist.ensure(sizeof(double) * std::max<int64_t>(ctx->t_total, 1)));
+  const double* d_rel[3] = {nullptr, nullptr, nullptr};
+  const int32_t* d_cell[3] = {nullptr, nullptr, nullptr};
+  for (int k = 0; k < grid->dim; ++k) {
+    d_rel[k] = ctx->in_x[k].as<double>();
+    d_cell[k] = ctx->in_cell[k].as<int32_t>();
+  }
+  TRY(sphx_rcll_distances_device(ctx, grid, ctx->t_n, d_rel, d_cell, precision,
+                                 ctx->t_offsets.as<int64_t>(), ctx->t_items.as<int32_t>(),
+                                 ctx->t_dist.as<double>()));
+  if (ctx->t_total)
+    CK(cudaMemcpyAsync(dist, ctx->t_dist.p, sizeof(double) * ctx->t_total, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return SPHX_OK;
+}
 
 int sphx_rcll_rows_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
                           const double* const d_rel[3], const int32_t* const d_cell[3],

@@ -1691,7 +1691,6 @@ __global__ void __launch_bounds__(EncShape<D, P>::BT) k_encode_rows(EncArgs e, S
       if (Lr == 0) pos += lt[2] + lt3;              // cells u+1, u+2
       else if (Lr == 1) pos += lt[1] + lt[2];       // cells u-1, u+1
       else pos += lt[0] + lt[1];                    // cells u-2, u-1
-      const int t = x0 + v - 2;
       const int64_t rec = rslot[v - 2] + pos;
       T cx = c[0];
       if constexpr (MODE == MODE_CLL) {
