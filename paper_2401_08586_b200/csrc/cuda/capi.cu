@@ -308,6 +308,7 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
   out->row0 = (int)sel.row0;
   out->nrows = (int)nrows;
   out->ids = sel.ids;
+  out->order = items;
   out->offsets = d_off;
   if (n == 0 || nrows == 0) {
     CK(cudaMemsetAsync(d_off, 0, sizeof(int64_t), st));

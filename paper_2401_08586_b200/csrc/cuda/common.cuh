@@ -51,6 +51,7 @@ struct SweepArgs {
   int64_t capacity;
   int row0, nrows;            // rows produced: particles [row0, row0 + nrows)
   const int32_t* ids;         // output id of particle j (null: j) -- global ids of a slab
+  const int32_t* order;       // CellGrid::items: the test kernel visits rows in cell order
   unsigned long long* tiles;  // [tiles] look-back words (epoch-tagged, never cleared)
   unsigned long long* ticket; // tile ticket counter (monotone across calls)
   unsigned long long tick0;   // ticket value at this call's first tile

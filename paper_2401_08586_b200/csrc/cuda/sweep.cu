@@ -1014,12 +1014,17 @@ __device__ __forceinline__ void r16_for_slots(F&& f) {
   }
 }
 
+// Rows are visited in cell (CSR) order, so the lanes of a warp are particles of
+// two or three cells that share their runs: the candidate loads of those lanes
+// coalesce and their loops run in step.
 template <int D>
 __global__ void __launch_bounds__(R16Two<D>::TB, R16Two<D>::TMINB) k_r16_test(SweepArgs a) {
   constexpr int NR = R16<D>::NR, W = R16Two<D>::W;
-  const int r = blockIdx.x * R16Two<D>::TB + threadIdx.x;
-  if (r >= a.nrows) return;
-  const int i = a.row0 + r;
+  const int t = blockIdx.x * R16Two<D>::TB + threadIdx.x;
+  if (t >= a.n) return;
+  const int i = a.order ? __ldg(a.order + t) : t;
+  const int r = i - a.row0;
+  if (r < 0 || r >= a.nrows) return;  // not a requested row (or malformed membership)
   const char* __restrict__ qc = static_cast<const char*>(a.qc);
   R16Own<D> own;
   own.init(a, i);
@@ -1822,7 +1827,7 @@ static int64_t sweep_t(const SweepArgs& a, cudaStream_t st) {
   if constexpr (P == FP16 && M == MODE_RCLL && D == 3) {
     // 3-D: tests and ordered emission in separate kernels (R16Two)
     using R = R16Two<D>;
-    k_r16_test<D><<<(unsigned)((a.nrows + R::TB - 1) / R::TB), R::TB, 0, st>>>(a);
+    k_r16_test<D><<<(unsigned)((a.n + R::TB - 1) / R::TB), R::TB, 0, st>>>(a);
     const int64_t nb = (a.nrows + R::BT - 1) / R::BT;
     k_r16_emit<D, R::BT, R::PCAP><<<(unsigned)nb, R::BT, 0, st>>>(a);
     return nb;
