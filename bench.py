@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--precision", default="fp16", choices=sorted(PREC))
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--op", default="table", choices=["table", "grad"],
+                    help="table: the NNPS table (default); grad: fused FP16 RCLL -> "
+                         "grad_normalized (SURVEY 8(f) row 1), no table in HBM")
     ap.add_argument("--slab", action="store_true",
                     help="use the slab-decomposed (multi-GPU) path even at N=1")
     return ap.parse_args()
@@ -340,6 +343,8 @@ def run_ours(args):
     start = torch.empty(C + 1, dtype=torch.int32, device=dev)
     items = torch.empty(n, dtype=torch.int32, device=dev)
     ctx.build_rel_coords_device(grid, xd, rel, cell, cell_of, start, items)
+    if args.op == "grad":
+        return bench_grad(args, w, ctx, stream, grid, n, C, xd, rel, cell, items, start, local)
     del xd
     offsets = torch.empty(n + 1, dtype=torch.int64, device=dev)
     cap = n * (24 if dim == 2 else 60)
@@ -478,6 +483,72 @@ def run_ours(args):
             line["cpu_baseline"] = cb
         else:
             line["cpu_baseline"] = cpu_baseline(args.config, args.precision)
+    print(json.dumps(line), flush=True)
+
+
+def bench_grad(args, w, ctx, stream, grid, n, C, xd, rel, cell, items, start, local):
+    """Fused FP16 RCLL -> grad_normalized: one step = the encode plus the fused kernel
+    on device-resident inputs (the table never reaches HBM). Parity: the whole
+    gradient field and degenerate count against the oracle on the same inputs."""
+    import torch
+
+    import oracle as O
+    dev = xd[0].device
+    dim, ds = w["dim"], w["ds"]
+    h = 1.2 * ds
+    f = torch.sin(7.0 * xd[0]) * torch.cos(5.0 * xd[dim - 1]) + xd[0] ** 2
+    g = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(dim)]
+    deg = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def step():
+        ctx.rcll_grad_normalized_device(grid, rel, cell, items, start, 2, xd, f, h, g, deg)
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    launches0 = ctx.launches
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    t = statistics.mean(a.elapsed_time(b) for a, b in ev) * 1e-3
+    # parity: the oracle's grad_normalized on the oracle's FP16 RCLL table
+    orc = O.Oracle()
+    xh = [a.cpu().numpy() for a in xd]
+    og = orc.grid(dim, 2.0 * h)
+    orel, ocell, _, ostart, oitems = orc.build_rel(og, xh)
+    tab = orc.rcll(og, orel, ocell, oitems, ostart, 2)
+    want, wdeg = orc.grad_normalized(dim, xh, f.cpu().numpy(), tab.offsets, tab.items, h)
+    exact = all(np.array_equal(g[k].cpu().numpy(), want[k]) for k in range(dim))
+    exact = exact and int(deg.item()) == wdeg
+    s_pos = 2 * dim
+    b_in = n * s_pos + 4 * n + 4 * (C + 1) + 8 * dim * n + 8 * n  # rel16 runs, ids, CSR, x, f
+    b_out = 8 * dim * n + 8
+    peak, peak_kind = measured_peaks()
+    line = {
+        "metric": "fused FP16 RCLL -> grad_normalized particles/s", "value": n / t,
+        "unit": "particles/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f16 search, f64 gradient", "data": "synthetic",
+        "config": {"workload": w["desc"] + " + grad_normalized (SURVEY 8(f) row 1)",
+                   "n_particles": n, "pairs_not_materialised": tab.total,
+                   "l2": "flushed between timed steps"},
+        "parity": {"bit_exact_vs_oracle": bool(exact), "degenerate": int(deg.item())},
+        "roofline": {"bound": "hbm", "kernel": "k_encode_rows + k_r16_grad",
+                     "achieved": (b_in + b_out) / t / 1e9, "peak": peak, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": (b_in + b_out) / t / 1e9 / peak,
+                     "algorithmic_bytes": b_in + b_out,
+                     "note": "the table (4P bytes) is never written: input-bound"},
+        "gpu_launches": ctx.launches - launches0,
+        "clocks": clk.summary(),
+    }
     print(json.dumps(line), flush=True)
 
 

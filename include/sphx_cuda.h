@@ -20,6 +20,9 @@
  *   sphx_rebuild_members <- void CellGrid::rebuild_members(const RelCoords&)
  *                                                                   cell_grid.hpp:150, cell_grid.cpp:86-108
  *   sphx_table_copy      <- (ownership hand-off of the returned NeighborTable, nnps.hpp:16-26)
+ *   sphx_rcll_grad_normalized(_device)
+ *                        <- grad_normalized(f, ps, rcll(rc, grid, fp16), kp) fused
+ *                                                                   gradient.cpp:44-82, dynamics.cpp:145-155
  *   sphx_table_distances / sphx_rcll_distances_device
  *                        <- double rel_distance(const RelCoords&, size_t i, size_t j,
  *                                               const CellGrid&, Precision) for every entry
@@ -208,6 +211,26 @@ int sphx_rcll_distances_device(sphx_context* ctx, const sphx_grid_desc* grid, in
  * inputs); dist receives sphx_rcll's *total doubles (host memory, synchronous). */
 int sphx_table_distances(sphx_context* ctx, const sphx_grid_desc* grid, int32_t precision,
                          double* dist);
+
+/* Fused FP16 RCLL -> grad_normalized: the mixed step's
+ *   grad_normalized(f, ps, rcll(rel, grid, fp16), make_kernel(h, dim))
+ * (dynamics.cpp:145-155, gradient.hpp:27, gradient.cpp:44-82, kernel.hpp:17-64)
+ * without materialising the neighbour table. g[k] receives GradField::g[k] (n
+ * doubles, particle order) and *degenerate GradField::degenerate_count; both are
+ * bit-identical to the reference. x[k] = ParticleSystem::x(k), f the field.
+ * precision must be SPHX_FP16 and dim 2 or 3. */
+int sphx_rcll_grad_normalized(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                              const double* const rel[3], const int32_t* const cell[3],
+                              int64_t n_items, const int32_t* items, const int32_t* cell_start,
+                              int32_t precision, const double* const x[3], const double* f,
+                              double h, double* const g[3], int64_t* degenerate);
+/* Device-memory variant (stream-ordered); *d_degenerate is overwritten. */
+int sphx_rcll_grad_normalized_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                                     const double* const d_rel[3], const int32_t* const d_cell[3],
+                                     const int32_t* d_items, const int32_t* d_cell_start,
+                                     int32_t precision, const double* const d_x[3],
+                                     const double* d_f, double h, double* const d_g[3],
+                                     unsigned long long* d_degenerate);
 
 /* Un-jittered build_lattice sites with ids [id0, id0 + count) written to d_x
  * (x_k = lo_k + (c_k + 0.5) ds, bit-identical to particle_system.cpp:53). */

@@ -127,6 +127,7 @@ def _bind_ref(lib):
             "ref_table_copy": (None, [vp, vp, vp]),
             "ref_table_hash": (C.c_uint64, [vp]),
             "ref_free_table": (None, [vp]),
+            "ref_grad_normalized": (C.c_int64, [vp, vp, vp, C.c_double, vp, vp, vp]),
             "ref_time_nnps": (C.c_double, [C.c_int, vp, vp, vp, C.c_int, C.c_int]),
         }
         for name, (res, args) in sig.items():
@@ -301,6 +302,19 @@ class RefSystem:
         return float(self.lib.ref_rel_distance(self.rel, self.grid, i, j, prec))
 
     # backends ----------------------------------------------------------------------
+    def grad_normalized_rcll(self, prec, f, h):
+        """The reference's mixed step core: grad_normalized(f, ps, rcll(rel, grid, prec),
+        make_kernel(h, dim)) (dynamics.cpp:145-155, gradient.cpp:44-82)."""
+        t = self.lib.ref_rcll(self.rel, self.grid, prec)
+        if not t:
+            raise RefError(self.lib.ref_last_error().decode())
+        f = np.ascontiguousarray(f, np.float64)
+        g = [np.zeros(self.n, np.float64) for _ in range(3)]
+        deg = self.lib.ref_grad_normalized(self.ps, t, f.ctypes.data, h,
+                                           *[a.ctypes.data for a in g])
+        self.lib.ref_free_table(t)
+        return g[:self.dim], int(deg)
+
     def rcll(self, prec) -> Table:
         return _ref_table(self.lib.ref_rcll(self.rel, self.grid, prec), self.lib)
 
@@ -365,6 +379,8 @@ def _oracle_lib():
             "so_rel_distance": (C.c_double, [C.POINTER(SoGrid), C.POINTER(vp), C.POINTER(vp),
                                              C.c_int64, C.c_int64, C.c_int]),
             "so_table_free": (None, [C.POINTER(_SoTable)]),
+            "so_grad_normalized": (C.c_int64, [C.c_int, C.c_int64, C.POINTER(vp), vp, vp, vp,
+                                               C.c_double, C.POINTER(vp)]),
             "so_table_hash": (C.c_uint64, [C.POINTER(_SoTable)]),
         }
         for name, (res, args) in sig.items():
@@ -471,6 +487,19 @@ class Oracle:
         if self.lib.so_all_list(len(xs), len(xs[0]), _ptrs(xs), h, prec, C.byref(t)) != 0:
             raise ValueError("all_list needs at least one particle")
         return _take_table(t)
+
+    def grad_normalized(self, dim, x, f, offsets, items, h):
+        """grad_normalized on a table (gradient.cpp:44-82): (g[dim], degenerate)."""
+        n = len(offsets) - 1
+        x = [np.ascontiguousarray(a, np.float64) for a in x]
+        f = np.ascontiguousarray(f, np.float64)
+        off = np.ascontiguousarray(offsets, np.int64)
+        it = np.ascontiguousarray(items, np.int32)
+        g = [np.zeros(n, np.float64) for _ in range(dim)]
+        gp = (C.c_void_p * 3)(*([a.ctypes.data for a in g] + [None] * (3 - dim)))
+        deg = self.lib.so_grad_normalized(dim, n, _ptrs(x), f.ctypes.data, off.ctypes.data,
+                                          it.ctypes.data, h, gp)
+        return g, int(deg)
 
     def rel_distance(self, g: SoGrid, rel, cell, i, j, prec) -> float:
         rel = [np.ascontiguousarray(a, np.float64) for a in rel]

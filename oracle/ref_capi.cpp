@@ -25,6 +25,7 @@
 #include "sphx/binary16.hpp"
 #include "sphx/cell_grid.hpp"
 #include "sphx/detail/nnps_batch.hpp"
+#include "sphx/gradient.hpp"
 #include "sphx/nnps.hpp"
 #include "sphx/particle_system.hpp"
 
@@ -284,6 +285,23 @@ void ref_table_copy(void* t, std::int64_t* offsets, std::int32_t* items) {
 }
 std::uint64_t ref_table_hash(void* t) { return fnv_table(*static_cast<sphx::NeighborTable*>(t)); }
 void ref_free_table(void* t) { delete static_cast<sphx::NeighborTable*>(t); }
+
+// ---- gradient on a table (gradient.hpp:27, gradient.cpp:44-82) ------------------------
+std::int64_t ref_grad_normalized(void* ps, void* t, const double* f, double h, double* g0,
+                                 double* g1, double* g2) {
+  std::int64_t deg = -1;
+  guarded([&] {
+    const auto& p = *static_cast<sphx::ParticleSystem*>(ps);
+    std::vector<double> fv(f, f + p.size());
+    const auto gf = sphx::grad_normalized(fv, p, *static_cast<sphx::NeighborTable*>(t),
+                                          sphx::make_kernel(h, p.dim()));
+    double* out[3] = {g0, g1, g2};
+    for (int k = 0; k < p.dim(); ++k)
+      if (out[k]) std::copy(gf.g[k].begin(), gf.g[k].end(), out[k]);
+    deg = gf.degenerate_count;
+  });
+  return deg;
+}
 
 // ---- timing (experiments.cpp:268-278 method: one discarded warm-up, median) -------------
 // which: 0 = rcll(rel, grid, prec), 1 = cell_link_list(ps, grid, prec).

@@ -600,3 +600,62 @@ double so_rel_distance(const so_grid* g, const double* const* rel, const int32_t
   }
   return so_round16(sqrt(acc));
 }
+
+/* ---- SPH gradient on a neighbour table (test infrastructure) --------------------
+ * make_kernel (kernel.hpp:17-29), kernel_dwdr (kernel.hpp:41-49), kernel_grad
+ * (kernel.hpp:53-64) and grad_normalized (gradient.cpp:44-82): FP64, each row
+ * summed in table order, built without contraction like the reference. */
+static double so_kernel_alpha(int dim, double h) {
+  const double pi = 3.14159265358979323846; /* std::numbers::pi */
+  if (dim == 1) return 1.0 / h;
+  if (dim == 2) return 15.0 / (7.0 * pi * h * h);
+  return 3.0 / (2.0 * pi * h * h * h);
+}
+
+static double so_kernel_dwdr(double R, double alpha) {
+  if (R < 1.0) return alpha * (-2.0 * R + 1.5 * R * R);
+  if (R < 2.0) {
+    const double t = 2.0 - R;
+    return -alpha * (0.5 * t * t);
+  }
+  return 0.0;
+}
+
+int64_t so_grad_normalized(int dim, int64_t n, const double* const* x, const double* f,
+                           const int64_t* offsets, const int32_t* items, double h,
+                           double** g) {
+  const double alpha = so_kernel_alpha(dim, h);
+  int64_t degenerate = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    double num[3] = {0.0, 0.0, 0.0}, den[3] = {0.0, 0.0, 0.0}, scale[3] = {0.0, 0.0, 0.0};
+    for (int64_t e = offsets[i]; e < offsets[i + 1]; ++e) {
+      const int32_t j = items[e];
+      double dx[3] = {0.0, 0.0, 0.0};
+      for (int k = 0; k < dim; ++k) dx[k] = x[k][i] - x[k][j];
+      double gw[3] = {0.0, 0.0, 0.0};
+      double r2 = 0.0;
+      for (int k = 0; k < dim; ++k) r2 += dx[k] * dx[k];
+      const double r = sqrt(r2);
+      if (r != 0.0) {
+        const double R = r / h;
+        const double sc = so_kernel_dwdr(R, alpha) / (h * r);
+        for (int k = 0; k < dim; ++k) gw[k] = sc * dx[k];
+      }
+      const double df = f[j] - f[i];
+      for (int k = 0; k < dim; ++k) {
+        num[k] += df * gw[k];
+        den[k] += -dx[k] * gw[k];
+        scale[k] += fabs(dx[k] * gw[k]);
+      }
+    }
+    for (int k = 0; k < dim; ++k) {
+      if (fabs(den[k]) < 1e-14 * (scale[k] > 0.0 ? scale[k] : 1.0)) {
+        g[k][i] = 0.0;
+        ++degenerate;
+      } else {
+        g[k][i] = num[k] / den[k];
+      }
+    }
+  }
+  return degenerate;
+}

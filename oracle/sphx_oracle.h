@@ -90,6 +90,13 @@ int so_all_list(int dim, int64_t n, const double* const* x, double h, int prec, 
 double so_rel_distance(const so_grid* g, const double* const* rel, const int32_t* const* cell,
                        int64_t i, int64_t j, int prec);
 
+/* grad_normalized (gradient.cpp:44-82) with the cubic B-spline gradient
+ * (kernel.hpp:17-64): g[k][i] for every row of the table; returns the number of
+ * degenerate (particle, axis) pairs. */
+int64_t so_grad_normalized(int dim, int64_t n, const double* const* x, const double* f,
+                           const int64_t* offsets, const int32_t* items, double h,
+                           double** g);
+
 #ifdef __cplusplus
 }
 #endif

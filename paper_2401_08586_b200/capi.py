@@ -94,6 +94,10 @@ def lib():
                                           p3]),
         "sphx_rcll_distances_device": (C.c_int, [vp, G, i64, p3, p3, i32, vp, vp, vp]),
         "sphx_table_distances": (C.c_int, [vp, G, i32, vp]),
+        "sphx_rcll_grad_normalized": (C.c_int, [vp, G, i64, p3, p3, i64, vp, vp, i32, p3, vp, dbl,
+                                                p3, C.POINTER(i64)]),
+        "sphx_rcll_grad_normalized_device": (C.c_int, [vp, G, i64, p3, p3, vp, vp, i32, p3, vp,
+                                                       dbl, p3, vp]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -110,7 +114,8 @@ EXPORTED = ("sphx_last_error", "sphx_grid_init", "sphx_create", "sphx_destroy",
             "sphx_build_rel_coords_device", "sphx_rebin_device", "sphx_enable_timing",
             "sphx_last_timing", "sphx_build_lattice", "sphx_build_random_uniform",
             "sphx_table_hash", "sphx_build_rel_coords_window_device", "sphx_rcll_rows_device",
-            "sphx_lattice_device", "sphx_rcll_distances_device", "sphx_table_distances")
+            "sphx_lattice_device", "sphx_rcll_distances_device", "sphx_table_distances",
+            "sphx_rcll_grad_normalized", "sphx_rcll_grad_normalized_device")
 
 
 def table_hash(offsets: np.ndarray, items: np.ndarray) -> int:
@@ -253,6 +258,32 @@ class Context:
                               items.ctypes.data, cell_start.ctypes.data, prec, C.byref(tot)))
         self._last_total = tot.value
         return self._fetch(n, tot.value)
+
+    def rcll_grad_normalized(self, grid: GridDesc, rel, cell, items, cell_start, prec: int, x, f,
+                             h: float):
+        """Fused grad_normalized(f, ps, rcll(rel, grid, prec), make_kernel(h, dim))."""
+        rel = [_c64(a) for a in rel]
+        cell = [_c32(a) for a in cell]
+        x = [_c64(a) for a in x]
+        f = _c64(f)
+        items = _c32(items)
+        cell_start = _c32(cell_start)
+        n = len(rel[0])
+        g = [np.empty(n, np.float64) for _ in range(len(rel))]
+        deg = C.c_int64()
+        check(lib().sphx_rcll_grad_normalized(self.h, C.byref(grid), n, _ptr3(rel), _ptr3(cell),
+                                              len(items), items.ctypes.data, cell_start.ctypes.data,
+                                              prec, _ptr3(x), f.ctypes.data, float(h), _ptr3(g),
+                                              C.byref(deg)))
+        return g, deg.value
+
+    def rcll_grad_normalized_device(self, grid, rel, cell, items, cell_start, prec, x, f, h, g,
+                                    deg):
+        self._bind(f)
+        check(lib().sphx_rcll_grad_normalized_device(
+            self.h, C.byref(grid), rel[0].numel(), _dptr3(rel), _dptr3(cell), items.data_ptr(),
+            cell_start.data_ptr(), prec, _dptr3(x), f.data_ptr(), float(h), _dptr3(g),
+            deg.data_ptr()))
 
     def table_distances(self, grid: GridDesc, prec: int) -> np.ndarray:
         """Per-pair distances of the last rcll() table (rel_distance per entry)."""

@@ -34,6 +34,7 @@ void launch_scan_counts(const int32_t* in, int32_t* out, int64_t C, unsigned lon
                         int* counter, cudaStream_t st);
 void launch_scatter_sort(int n, int64_t C, const int32_t* cell_of, const int32_t* slot,
                          const int32_t* start, int32_t* items, cudaStream_t st);
+int launch_rcll_grad(int dim, const SweepArgs& a, cudaStream_t st);
 int launch_rcll_distances(int dim, int prec, int64_t nrows, const GridConsts& g,
                           const PrecConsts& pc, const double hc[3], const double* const rel[3],
                           const int32_t* const cell[3], const int64_t* off,
@@ -129,6 +130,8 @@ struct sphx_context {
   int64_t sw_ntiles = 0;
   // table of the last host-API call
   Buf t_offsets, t_items, t_dist;
+  // fused gradient (host API staging)
+  Buf g_x[3], g_f, g_out[3], g_deg;
   int64_t t_n = -1, t_total = 0, t_capacity = 0;
   bool t_rcll = false;  // the last host table came from sphx_rcll (inputs still staged)
   // binning scratch
@@ -563,7 +566,8 @@ void sphx_destroy(sphx_context* ctx) {
   Buf* all[] = {&ctx->in_x[0], &ctx->in_x[1], &ctx->in_x[2], &ctx->in_cell[0], &ctx->in_cell[1],
                 &ctx->in_cell[2], &ctx->in_items, &ctx->in_start, &ctx->in_cellof, &ctx->pos_own,
                 &ctx->tri, &ctx->pos_csr, &ctx->cell_slot, &ctx->qc,
-                &ctx->qtag, &ctx->selfpos, &ctx->sw_tiles, &ctx->sw_ticket, &ctx->sw_rowk, &ctx->sw_hitw, &ctx->t_offsets, &ctx->t_items, &ctx->t_dist,
+                &ctx->qtag, &ctx->selfpos, &ctx->sw_tiles, &ctx->sw_ticket, &ctx->sw_rowk, &ctx->sw_hitw, &ctx->t_offsets, &ctx->t_items, &ctx->t_dist, &ctx->g_x[0], &ctx->g_x[1], &ctx->g_x[2],
+                &ctx->g_f, &ctx->g_out[0], &ctx->g_out[1], &ctx->g_out[2], &ctx->g_deg,
                 &ctx->b_counts, &ctx->b_slot, &ctx->b_bad, &ctx->b_tiles, &ctx->b_out_cellof,
                 &ctx->b_out_start, &ctx->b_out_items, &ctx->b_rel[0], &ctx->b_rel[1],
                 &ctx->b_rel[2], &ctx->b_cell[0], &ctx->b_cell[1], &ctx->b_cell[2]};
@@ -811,6 +815,83 @@ int sphx_rebin_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
 }
 
 // ---------------- multi-GPU slab path ----------------
+
+int sphx_rcll_grad_normalized_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                                     const double* const d_rel[3], const int32_t* const d_cell[3],
+                                     const int32_t* d_items, const int32_t* d_cell_start,
+                                     int32_t precision, const double* const d_x[3],
+                                     const double* d_f, double h, double* const d_g[3],
+                                     unsigned long long* d_degenerate) {
+  TRY(check_ctx(ctx));
+  if (!grid) return fail(SPHX_ERR_INVALID_ARGUMENT, "null grid");
+  TRY(check_prec_dim(precision, grid->dim));
+  if (precision != SPHX_FP16 || grid->dim < 2)
+    return fail(SPHX_ERR_INVALID_ARGUMENT,
+                "the fused gradient runs on the FP16 RCLL search in 2-D or 3-D");
+  if (!(h > 0.0)) return fail(SPHX_ERR_INVALID_ARGUMENT, "smoothing length must be positive");
+  if (n == 0) return SPHX_OK;
+  SweepArgs a;
+  TRY(ctx->t_offsets.ensure(sizeof(int64_t) * (n + 1)));
+  TRY(run_prepare(ctx, MODE_RCLL, *grid, n, d_rel, d_cell, d_items, d_cell_start, nullptr,
+                  precision, 0.0, ctx->t_offsets.as<int64_t>(), &a));
+  for (int k = 0; k < 3; ++k) {
+    a.gx[k] = k < grid->dim ? d_x[k] : nullptr;
+    a.gout[k] = k < grid->dim ? d_g[k] : nullptr;
+  }
+  a.gf = d_f;
+  a.gdeg = d_degenerate;
+  a.gh = h;
+  // make_kernel (kernel.hpp:17-29), evaluated as the reference writes it
+  const double pi = 3.141592653589793;
+  a.galpha = grid->dim == 2 ? 15.0 / (7.0 * pi * h * h) : 3.0 / (2.0 * pi * h * h * h);
+  CK(cudaMemsetAsync(d_degenerate, 0, sizeof(unsigned long long), ctx->stream));
+  ctx->launches += launch_rcll_grad(grid->dim, a, ctx->stream);
+  CKL();
+  if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], ctx->stream));
+  return SPHX_OK;
+}
+
+int sphx_rcll_grad_normalized(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                              const double* const rel[3], const int32_t* const cell[3],
+                              int64_t n_items, const int32_t* items, const int32_t* cell_start,
+                              int32_t precision, const double* const x[3], const double* f,
+                              double h, double* const g[3], int64_t* degenerate) {
+  TRY(check_ctx(ctx));
+  if (!grid || !degenerate) return fail(SPHX_ERR_INVALID_ARGUMENT, "null argument");
+  TRY(check_prec_dim(precision, grid->dim));
+  if (n_items != n) return fail(SPHX_ERR_INVALID_ARGUMENT, "grid membership is stale");
+  const int dim = grid->dim;
+  const int64_t C = cell_total(*grid);
+  const double* d_rel[3] = {nullptr, nullptr, nullptr};
+  const int32_t* d_cell[3] = {nullptr, nullptr, nullptr};
+  const double* d_x[3] = {nullptr, nullptr, nullptr};
+  double* d_g[3] = {nullptr, nullptr, nullptr};
+  for (int k = 0; k < dim; ++k) {
+    TRY(upload(ctx, ctx->in_x[k], rel[k], sizeof(double) * n));
+    TRY(upload(ctx, ctx->in_cell[k], cell[k], sizeof(int32_t) * n));
+    TRY(upload(ctx, ctx->g_x[k], x[k], sizeof(double) * n));
+    TRY(ctx->g_out[k].ensure(sizeof(double) * std::max<int64_t>(n, 1)));
+    d_rel[k] = ctx->in_x[k].as<double>();
+    d_cell[k] = ctx->in_cell[k].as<int32_t>();
+    d_x[k] = ctx->g_x[k].as<double>();
+    d_g[k] = ctx->g_out[k].as<double>();
+  }
+  TRY(upload(ctx, ctx->in_items, items, sizeof(int32_t) * n));
+  TRY(upload(ctx, ctx->in_start, cell_start, sizeof(int32_t) * (C + 1)));
+  TRY(upload(ctx, ctx->g_f, f, sizeof(double) * n));
+  TRY(ctx->g_deg.ensure(sizeof(unsigned long long)));
+  TRY(sphx_rcll_grad_normalized_device(ctx, grid, n, d_rel, d_cell, ctx->in_items.as<int32_t>(),
+                                       ctx->in_start.as<int32_t>(), precision, d_x,
+                                       ctx->g_f.as<double>(), h, d_g,
+                                       ctx->g_deg.as<unsigned long long>()));
+  for (int k = 0; k < dim; ++k)
+    if (n) CK(cudaMemcpyAsync(g[k], d_g[k], sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  unsigned long long deg = 0;
+  if (n) CK(cudaMemcpyAsync(&deg, ctx->g_deg.p, sizeof(deg), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *degenerate = (int64_t)deg;
+  return SPHX_OK;
+}
 
 int sphx_rcll_distances_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
                                const double* const d_rel[3], const int32_t* const d_cell[3],

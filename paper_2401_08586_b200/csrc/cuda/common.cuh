@@ -52,6 +52,12 @@ struct SweepArgs {
   int row0, nrows;            // rows produced: particles [row0, row0 + nrows)
   const int32_t* ids;         // output id of particle j (null: j) -- global ids of a slab
   const int32_t* order;       // CellGrid::items: the test kernel visits rows in cell order
+  // fused NNPS -> grad_normalized (gradient.cpp:44-82)
+  const double* gx[3];        // ParticleSystem::x(k)
+  const double* gf;           // the field f
+  double* gout[3];            // GradField::g[k]
+  unsigned long long* gdeg;   // GradField::degenerate_count (accumulated)
+  double gh, galpha;          // KernelParams h, alpha (make_kernel, kernel.hpp:17-29)
   unsigned long long* tiles;  // [tiles] look-back words (epoch-tagged, never cleared)
   unsigned long long* ticket; // tile ticket counter (monotone across calls)
   unsigned long long tick0;   // ticket value at this call's first tile

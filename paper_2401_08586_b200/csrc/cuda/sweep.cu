@@ -1120,6 +1120,169 @@ __global__ void __launch_bounds__(BT, R16Two<D>::EMINB) k_r16_emit(SweepArgs a) 
   stream_tile<BT>(gout, SharedRow{(uint32_t)__cvta_generic_to_shared(PK)}, btot, tid);
 }
 
+// ------------------------------------------------------------------------------
+// Fused FP16 RCLL -> grad_normalized (the mixed step's core,
+// dynamics.cpp:145-155): the neighbour rows never reach HBM. Rows are visited in
+// cell order (lanes of a warp share runs); each row is built sorted in a per-thread
+// shared-memory slot exactly as the table would hold it, and the FP64 gradient is
+// accumulated over it in that order with explicit round-to-nearest operations, so
+// the result is bit-identical to grad_normalized(f, ps, rcll(rel, grid, fp16), kp):
+//   dx = x_i - x_j; r = sqrt(sum dx^2); R = r/h; dW/dR (kernel.hpp:41-49);
+//   gw = dW/dR / (h r) * dx (kernel.hpp:53-64); num += (f_j - f_i) gw;
+//   den += (-dx) gw; scale += |dx gw|; g = num/den, or 0 (degenerate) when
+//   |den| < 1e-14 * (scale > 0 ? scale : 1) (gradient.cpp:56-79).
+// A row longer than the slot is walked in id order by repeated minimum search.
+// ------------------------------------------------------------------------------
+template <int D>
+struct R16Grad {
+  static constexpr int BT = D == 3 ? 64 : 128;
+  static constexpr int CAP = D == 3 ? 80 : 24;  // row slot
+  static constexpr int W = D == 3 ? 16 : 4;     // hit words kept
+};
+
+__device__ __forceinline__ double kdwdr(double R, double alpha) {
+  if (R < 1.0) return __dmul_rn(alpha, __dadd_rn(__dmul_rn(-2.0, R), __dmul_rn(__dmul_rn(1.5, R), R)));
+  if (R < 2.0) {
+    const double t = __dsub_rn(2.0, R);
+    return __dmul_rn(-alpha, __dmul_rn(__dmul_rn(0.5, t), t));
+  }
+  return 0.0;
+}
+
+template <int D>
+struct GradAcc {
+  double num[3] = {0.0, 0.0, 0.0}, den[3] = {0.0, 0.0, 0.0}, scale[3] = {0.0, 0.0, 0.0};
+  double xi[3], fi;
+  __device__ __forceinline__ void add(const SweepArgs& a, int j) {
+    double dx[3], gw[3] = {0.0, 0.0, 0.0}, r2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      dx[k] = __dsub_rn(xi[k], __ldg(a.gx[k] + j));
+      r2 = __dadd_rn(r2, __dmul_rn(dx[k], dx[k]));
+    }
+    const double r = __dsqrt_rn(r2);
+    if (r != 0.0) {
+      const double R = __ddiv_rn(r, a.gh);
+      const double sc = __ddiv_rn(kdwdr(R, a.galpha), __dmul_rn(a.gh, r));
+#pragma unroll
+      for (int k = 0; k < D; ++k) gw[k] = __dmul_rn(sc, dx[k]);
+    }
+    const double df = __dsub_rn(__ldg(a.gf + j), fi);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      num[k] = __dadd_rn(num[k], __dmul_rn(df, gw[k]));
+      den[k] = __dadd_rn(den[k], __dmul_rn(-dx[k], gw[k]));
+      scale[k] = __dadd_rn(scale[k], fabs(__dmul_rn(dx[k], gw[k])));
+    }
+  }
+};
+
+template <int D, int BT, int CAP, int W>
+__global__ void __launch_bounds__(BT) k_r16_grad(SweepArgs a) {
+  constexpr int NR = R16<D>::NR;
+  __shared__ __align__(16) int32_t ROWS[BT * CAP];
+  __shared__ unsigned NIB[W * BT];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int t = blockIdx.x * BT + tid;
+  const bool active = t < a.n;
+  const int i = active ? (a.order ? __ldg(a.order + t) : t) : 0;
+  const char* __restrict__ qc = static_cast<const char*>(a.qc);
+  const uint4* __restrict__ tags = reinterpret_cast<const uint4*>(a.qtag);
+  const int32_t* __restrict__ tag1 = reinterpret_cast<const int32_t*>(a.qtag);
+  unsigned long long deg = 0;
+  if (active) {
+    R16Own<D> own;
+    own.init(a, i);
+    int cb[NR], ce[NR];
+    r16_runs<D>(a, i, true, cb, ce);
+    // A: hit words
+    int k = 0, w = 0;
+    r16_for_slots<D, 0>([&](auto qv) {
+      constexpr int Q = decltype(qv)::value;
+      for (int g = cb[Q]; g < ce[Q]; g += 8) {
+        const unsigned word = own.template group<Q>(qc, g, min(g + 8, ce[Q]));
+        k += __popc(word);
+        if (w < W) NIB[w * BT + tid] = word;
+        ++w;
+      }
+    });
+    auto word_at = [&](int wi, auto qv, int g) -> unsigned {
+      constexpr int Q = decltype(qv)::value;
+      return wi < W ? NIB[wi * BT + tid] : own.template group<Q>(qc, g, min(g + 8, ce[Q]));
+    };
+    GradAcc<D> acc;
+#pragma unroll
+    for (int kk = 0; kk < D; ++kk) acc.xi[kk] = __ldg(a.gx[kk] + i);
+    acc.fi = __ldg(a.gf + i);
+    if (k <= CAP) {
+      // B: the sorted row in this thread's slot, then the gradient over it
+      const SharedRow row{(uint32_t)__cvta_generic_to_shared(ROWS) + 4u * (uint32_t)(tid * CAP)};
+      int kk = 0, wq = 0;
+      r16_for_slots<D, 0>([&](auto qv) {
+        constexpr int Q = decltype(qv)::value;
+        const int gs = kk;
+        for (int g = cb[Q]; g < ce[Q]; g += 8) {
+          unsigned word = word_at(wq, qv, g);
+          ++wq;
+          for (int ch = g; word; ++ch, word >>= 4) {
+            const unsigned m = word & 15u;
+            if (m) append4(row, kk, m, __ldg(tags + ch));
+          }
+        }
+        if (gs > 0 && kk > gs && row.ld(gs) < row.ld(gs - 1)) merge_tail(row, gs, kk);
+      });
+      for (int e = 0; e < k; ++e) acc.add(a, row.ld(e));
+    } else {
+      // long row: ids in ascending order by repeated minimum search over the hits
+      int last = INT_MIN;
+      for (int e = 0; e < k; ++e) {
+        int best = INT_MAX, wq = 0;
+        r16_for_slots<D, 0>([&](auto qv) {
+          constexpr int Q = decltype(qv)::value;
+          for (int g = cb[Q]; g < ce[Q]; g += 8) {
+            unsigned word = word_at(wq, qv, g);
+            ++wq;
+            while (word) {
+              const int b = __ffs(word) - 1;
+              word &= word - 1;
+              const int id = __ldg(tag1 + 4 * (int64_t)g + b);
+              if (id > last && id < best) best = id;
+            }
+          }
+        });
+        acc.add(a, best);
+        last = best;
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < D; ++kk) {
+      const double lim = __dmul_rn(1e-14, acc.scale[kk] > 0.0 ? acc.scale[kk] : 1.0);
+      double g = 0.0;
+      if (fabs(acc.den[kk]) < lim) ++deg;
+      else g = __ddiv_rn(acc.num[kk], acc.den[kk]);
+      a.gout[kk][i] = g;
+    }
+  }
+  // degenerate pairs: warp sum, one atomic per warp
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) deg += __shfl_xor_sync(0xffffffffu, deg, o);
+  if (lane == 0 && deg) atomicAdd(a.gdeg, deg);
+}
+
+int launch_rcll_grad(int dim, const SweepArgs& a, cudaStream_t st) {
+  if (dim == 2) {
+    using G = R16Grad<2>;
+    k_r16_grad<2, G::BT, G::CAP, G::W><<<(unsigned)((a.n + G::BT - 1) / G::BT), G::BT, 0, st>>>(a);
+    return 1;
+  }
+  if (dim == 3) {
+    using G = R16Grad<3>;
+    k_r16_grad<3, G::BT, G::CAP, G::W><<<(unsigned)((a.n + G::BT - 1) / G::BT), G::BT, 0, st>>>(a);
+    return 1;
+  }
+  return 0;
+}
+
 // The whole table in one pass over tiles of BT consecutive rows (particle order).
 //   A. each thread tests its particle's candidates; the hit words go to shared
 //      memory (WMAX per thread; later groups are re-tested in B) and the row

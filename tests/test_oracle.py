@@ -166,3 +166,21 @@ def test_oracle_c2_golden(orc, be_prec):
         t = orc.cll(g, x, h, cell_of, items, start, PREC[prec])
     assert t.total == c["tables"][be_prec]["total"]
     assert f"{t.hash():016x}" == c["tables"][be_prec]["hash"]
+
+
+@pytest.mark.parametrize("dim,ds,jitter", [(2, 0.02, 0.3), (3, 0.1, 0.3), (2, 0.05, 0.0)])
+def test_oracle_grad_normalized_matches_reference(dim, ds, jitter):
+    """The oracle's grad_normalized restatement == the reference's gradient.cpp on the
+    reference's own FP16 RCLL table (the mixed step, dynamics.cpp:145-155)."""
+    if not os.path.exists(O.REF_SO):
+        pytest.skip("reference library not built")
+    r = O.RefSystem.lattice(dim, ds, jitter, 1).make_grid()
+    x = [r.x(k) for k in range(dim)]
+    h = 1.2 * ds
+    for f in (np.sin(3 * x[0]) + x[dim - 1] ** 2, 1.0 + 2.0 * x[0]):
+        gr, dr = r.grad_normalized_rcll(2, f, h)
+        t = r.rcll(2)
+        go, do = O.Oracle().grad_normalized(dim, x, f, t.offsets, t.items, h)
+        assert dr == do
+        for a, b in zip(gr, go):
+            assert np.array_equal(a, b)
