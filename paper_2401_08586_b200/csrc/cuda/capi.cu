@@ -19,8 +19,7 @@ namespace sphx_dev {
 // sweep.cu
 int launch_encode(int dim, int prec, int mode, int n, int64_t C, int nx, int wrapx,
                   const PrecConsts& pc, const double* const x[3], const int32_t* items,
-                  const int32_t* start, void* pos_csr, int32_t* cell_slot, const SweepArgs& a,
-                  cudaStream_t st);
+                  const int32_t* start, const SweepArgs& a, cudaStream_t st);
 int64_t launch_sweep(int dim, int prec, int mode, const SweepArgs& a, cudaStream_t st);
 size_t coord_bytes(int dim, int prec);
 size_t chunk_bytes(int dim, int prec, int mode);
@@ -122,7 +121,7 @@ struct sphx_context {
   // inputs staged from host
   Buf in_x[3], in_cell[3], in_items, in_start, in_cellof;
   // encode / sweep scratch
-  Buf pos_own, pos_csr, cell_slot, tri, qc, qtag, selfpos;
+  Buf pos_own, tri, qc, qtag, selfpos;
   // single-pass sweep: look-back words (epoch-tagged) and the tile ticket
   Buf sw_tiles, sw_ticket, sw_rowk, sw_hitw;
   unsigned long long sw_tick = 0;
@@ -323,8 +322,6 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
   TRY(ctx->qc.ensure(chunk_bytes(g.dim, prec, mode) * (size_t)chunks));
   TRY(ctx->qtag.ensure(16 * (size_t)chunks));
   if (mode != MODE_ALL) {
-    TRY(ctx->pos_csr.ensure(coord_bytes(g.dim, prec) * (size_t)n));
-    TRY(ctx->cell_slot.ensure(sizeof(int32_t) * (size_t)n));
     TRY(ctx->tri.ensure(sizeof(int2) * std::max<int64_t>(C, 1)));
     TRY(ctx->selfpos.ensure(sizeof(int32_t) * (size_t)n));
   }
@@ -343,8 +340,7 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
 
   if (ctx->timing) CK(cudaEventRecord(ctx->ev[0], st));
   ctx->launches += launch_encode(g.dim, prec, mode, n, C, a.g.counts[0], a.g.wrap[0], a.c, src,
-                                 items, start, ctx->pos_csr.p, ctx->cell_slot.as<int32_t>(), a,
-                                 st);
+                                 items, start, a, st);
   CKL();
   if (ctx->timing) CK(cudaEventRecord(ctx->ev[1], st));
   return SPHX_OK;
@@ -565,7 +561,7 @@ void sphx_destroy(sphx_context* ctx) {
   cudaStreamSynchronize(ctx->stream);
   Buf* all[] = {&ctx->in_x[0], &ctx->in_x[1], &ctx->in_x[2], &ctx->in_cell[0], &ctx->in_cell[1],
                 &ctx->in_cell[2], &ctx->in_items, &ctx->in_start, &ctx->in_cellof, &ctx->pos_own,
-                &ctx->tri, &ctx->pos_csr, &ctx->cell_slot, &ctx->qc,
+                &ctx->tri, &ctx->qc,
                 &ctx->qtag, &ctx->selfpos, &ctx->sw_tiles, &ctx->sw_ticket, &ctx->sw_rowk, &ctx->sw_hitw, &ctx->t_offsets, &ctx->t_items, &ctx->t_dist, &ctx->g_x[0], &ctx->g_x[1], &ctx->g_x[2],
                 &ctx->g_f, &ctx->g_out[0], &ctx->g_out[1], &ctx->g_out[2], &ctx->g_deg,
                 &ctx->b_counts, &ctx->b_slot, &ctx->b_bad, &ctx->b_tiles, &ctx->b_out_cellof,

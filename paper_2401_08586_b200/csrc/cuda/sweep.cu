@@ -9,20 +9,23 @@
 //   all_list        nnps.cpp:128-172
 //   build_table     nnps.cpp:26-66 (rows ascending, int64 offsets)
 //
-// Candidate layout ("x-triples" in 4-record chunks). For every cell c the encode
-// step merges, by particle id, the members of the x-neighbour cells (cx-1, cx,
-// cx+1) -- wrapped on a periodic x axis -- into one run of records, padded with
-// NaN sentinels to whole chunks of 4. Chunks are stored structure-of-arrays: one
-// quad of coordinates per axis (binary16 quad = 8 B), one quad of x offsets dc
-// (RCLL; dc = cx_i - cx_j in {-1,0,1}) and one quad of ids. CLL records carry the
-// periodic x shift already applied (round_to(prec, xj + shift), nnps.cpp:116).
-// A particle's candidates are the 3 (2-D) / 9 (3-D) runs of its (dy, dz) rows.
+// Candidate layout ("x-triple runs" in 4-record chunks). For every cell c the
+// encode (k_encode_rows) merges, by particle id, the members of the x-neighbour
+// cells (cx-1, cx, cx+1) -- wrapped on a periodic x axis -- into one run of
+// records, padded with NaN sentinels to whole chunks of 4. A chunk is one record
+// of quads (array of structures, 32 bytes at FP16): a quad of coordinates per
+// axis, then for RCLL the quad of x offsets dc = cx_i - cx_j in {-1,0,1}; the 4
+// ids of a chunk are a separate uint4. CLL records carry the periodic x shift
+// already applied (round_to(prec, xj + shift), nnps.cpp:116). A particle's
+// candidates are the 3 (2-D) / 9 (3-D) runs of its (dz, dy) rows.
 //
-// One pass (k_sweep) over tiles of consecutive rows (particle order): distance
-// tests of every candidate, sorted rows in shared memory, a block scan plus a
-// decoupled look-back for the row offsets, and 16-byte stores of the packed
-// tile. Consecutive particles share cells in lattice and cell-sorted orders, so
-// a tile's candidate loads are L1 hits; in any order they are L2 hits.
+// Kernels (each a tile of consecutive rows in particle order, a decoupled
+// look-back for the row offsets, sorted rows packed in shared memory, 16-byte
+// stores of the tile):
+//   k_rcll16<2>            FP16 RCLL 2-D, one fused pass;
+//   k_r16_test/k_r16_emit  FP16 RCLL 3-D, tests (cell order) and ordered emission;
+//   k_sweep<D,P,MODE>      every other precision / mode (one pass);
+//   k_r16_grad<D>          fused FP16 RCLL -> grad_normalized (no table).
 //
 // Bit-exactness: every step is an explicit round-to-nearest op in the
 // precision (no contraction; the reference is built without -march). The x term
@@ -1385,36 +1388,16 @@ __global__ void __launch_bounds__(BT) k_sweep(SweepArgs a) {
 // ------------------------------------------------------------------------------
 // Encode
 // ------------------------------------------------------------------------------
-// Own coordinates (particle order); for the cell modes also the members' packed coordinates in CSR order. RCLL: src = RelCoords::rel
-// (nnps.cpp:304-315); CLL/all: src = positions (round_coords nnps.cpp:75-89).
-template <int D, int P, int MODE>
-__global__ void k_encode_own(int n, const double* __restrict__ x0, const double* __restrict__ x1,
-                             const double* __restrict__ x2, const int32_t* __restrict__ items,
-                             void* __restrict__ pos_csr, int32_t* __restrict__ cell_slot,
-                             SweepArgs a) {
+// Own coordinates at storage precision, particle order (all_list: round_to,
+// nnps.cpp:75-89; the cell modes get theirs from k_encode_rows).
+template <int D, int P>
+__global__ void k_pack_own(int n, const double* __restrict__ x0, const double* __restrict__ x1,
+                           const double* __restrict__ x2, void* __restrict__ pos_own) {
   using C = typename Coord<D, P>::T;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   const double v[3] = {x0[t], D > 1 ? x1[t] : 0.0, D > 2 ? x2[t] : 0.0};
-  reinterpret_cast<C*>(const_cast<void*>(a.pos_own))[t] = pack<D, P>(v);
-  if constexpr (MODE != MODE_ALL) {
-    int j = items[t];
-    if (j < 0 || j >= n) j = 0;  // malformed membership: stay memory-safe
-    const double w[3] = {x0[j], D > 1 ? x1[j] : 0.0, D > 2 ? x2[j] : 0.0};
-    reinterpret_cast<C*>(pos_csr)[t] = pack<D, P>(w);
-    // the cell holding slot t: the member's own cell (RelCoords::cell for RCLL,
-    // CellGrid::cell_of for CLL), clamped to stay memory-safe
-    int c;
-    if constexpr (MODE == MODE_RCLL) {
-      int ck[3] = {0, 0, 0};
-#pragma unroll
-      for (int k = 0; k < D; ++k) ck[k] = min(max(a.cellk[k][j], 0), a.g.counts[k] - 1);
-      c = (ck[2] * a.g.counts[1] + ck[1]) * a.g.counts[0] + ck[0];
-    } else {
-      c = a.cell_of[j];
-    }
-    cell_slot[t] = c;
-  }
+  reinterpret_cast<C*>(pos_own)[t] = pack<D, P>(v);
 }
 
 // Chunk start of cell c's run: with st(x) = cell_start[row + x], n_x the cell
@@ -1436,127 +1419,10 @@ __device__ __forceinline__ int64_t run_record_slot(const int32_t* st, int cx, in
   return (A + 6 * c + 3) & ~int64_t(3);
 }
 
-// x-neighbour list l (0: cx-1, 1: cx, 2: cx+1) of the run centred at tx: its cell
-// range in the row, and the periodic wrap direction (-1: seen one period below).
-__device__ __forceinline__ int list_range(const int32_t* st, int tx, int l, int nx, int wrapx,
-                                          int& lo, int& hi) {
-  int x = tx - 1 + l, w = 0;
-  if (x < 0) {
-    if (!wrapx) return lo = hi = 0, 0;
-    x += nx;
-    w = -1;
-  } else if (x >= nx) {
-    if (!wrapx) return lo = hi = 0, 0;
-    x -= nx;
-    w = 1;
-  }
-  lo = st[x];
-  hi = st[x + 1];
-  return w;
-}
-
 // record r (chunk r/4, element r%4), quad q
 template <int D, int P, int MODE>
 __device__ __forceinline__ void store_el(void* qc, int64_t r, int q, typename Prec<P>::T v) {
   *rec_el<D, P, MODE>(qc, r >> 2, q, (int)(r & 3)) = v;
-}
-
-// One thread per cell c: the run's chunk range and the sentinel records (NaN
-// coordinates, id ~0) that pad it to whole chunks.
-template <int D, int P, int MODE>
-__global__ void k_encode_runs(int64_t C, int nx, int wrapx, const int32_t* __restrict__ start,
-                              SweepArgs a) {
-  using T = typename Prec<P>::T;
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  const int cx = (int)(c % nx);
-  const int32_t* st = start + (c - cx);
-  int len = 0;
-#pragma unroll
-  for (int l = 0; l < 3; ++l) {
-    int lo, hi;
-    list_range(st, cx, l, nx, wrapx, lo, hi);
-    len += hi - lo;
-  }
-  const int64_t slot = run_record_slot(st, cx, nx, wrapx, c);
-  const int nch = (len + 3) >> 2;
-  a.tri[c] = make_int2((int)(slot >> 2), (int)((slot >> 2) + nch));
-  T nan;
-  if constexpr (P == FP16) nan = hbits(0x7E00u); else nan = T(NAN);
-  for (int q = len; q < 4 * nch; ++q) {
-#pragma unroll
-    for (int k = 0; k < D; ++k) store_el<D, P, MODE>(a.qc, slot + q, k, nan);
-    if constexpr (MODE == MODE_RCLL) store_el<D, P, MODE>(a.qc, slot + q, D, T(0.0f));
-    reinterpret_cast<unsigned*>(a.qtag)[slot + q] = 0xFFFFFFFFu;
-  }
-}
-
-// One thread per CSR slot s (particle j = items[s] in cell c): its record in
-// each of the three runs that contain cell c (runs centred at cx+1, cx, cx-1,
-// where c is list 0, 1, 2). The record's place in a run is its index in c plus
-// the number of smaller ids in the run's two other cells (cells hold ascending
-// ids), i.e. the position in the id-merge of the three cells. With slab ids the
-// merge key is the output id (each cell is one id-ascending class there).
-template <int D, int P, int MODE>
-__global__ void k_encode_members(int n, int nx, int wrapx, PrecConsts pc,
-                                 const int32_t* __restrict__ start,
-                                 const int32_t* __restrict__ items,
-                                 const int32_t* __restrict__ cell_of_slot,
-                                 const void* __restrict__ pos_csr, SweepArgs a) {
-  using T = typename Prec<P>::T;
-  using CT = typename Coord<D, P>::T;
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n) return;
-  const int j = __ldg(items + s);
-  const int c = __ldg(cell_of_slot + s);
-  const int cx = c % nx;
-  const int32_t* st = start + (c - cx);
-  const int idx = s - __ldg(st + cx);
-  const CT cj = ldg<CT>(pos_csr, s);
-#pragma unroll
-  for (int L = 0; L < 3; ++L) {  // c is list L of the run centred at tx
-    int tx = cx + 1 - L;
-    if (tx < 0 || tx >= nx) {
-      if (!wrapx) continue;
-      tx = tx < 0 ? tx + nx : tx - nx;
-    }
-    int pos = idx, w = 0;
-#pragma unroll
-    for (int l = 0; l < 3; ++l) {
-      int lo, hi;
-      const int wl = list_range(st, tx, l, nx, wrapx, lo, hi);
-      if (l == L) {
-        w = wl;
-        continue;
-      }
-      int cnt = 0;
-      if (a.ids) {  // slab: merge by output (global) id -- in 1-D a run can mix
-        const int gj = __ldg(a.ids + j);  // owned and halo cells
-        for (int q = lo; q < hi; ++q) cnt += __ldg(a.ids + __ldg(items + q)) < gj;
-      } else {
-        for (int q = lo; q < hi; ++q) cnt += __ldg(items + q) < j;
-      }
-      pos += cnt;
-    }
-    const int64_t r = run_record_slot(st, tx, nx, wrapx, (c - cx) + tx) + pos;
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      T v = axis_of<D, P>(cj, k);
-      if (MODE == MODE_CLL && k == 0 && w != 0) {  // round_to(prec, xj + shift), nnps.cpp:116
-        T sh;
-        if constexpr (P == FP16) sh = hbits(pc.h_sh[0]);
-        else if constexpr (P == FP32) sh = pc.f_sh[0];
-        else sh = pc.d_sh[0];
-        if constexpr (P == FP16) v = __hadd_rn(v, w > 0 ? sh : __hneg(sh));
-        else v = f_add(v, w > 0 ? sh : -sh);
-      }
-      store_el<D, P, MODE>(a.qc, r, k, v);
-    }
-    if constexpr (MODE == MODE_RCLL) store_el<D, P, MODE>(a.qc, r, D, (T)(float)(1 - L));  // dc_x
-    // output id: the particle index, or its global id for a multi-GPU slab
-    reinterpret_cast<unsigned*>(a.qtag)[r] = a.ids ? (unsigned)__ldg(a.ids + j) : (unsigned)j;
-    if (L == 1) a.selfpos[j] = (int)r;
-  }
 }
 
 // all_list: chunks of 4 consecutive particles (one run over everything).
@@ -1929,12 +1795,9 @@ __global__ void __launch_bounds__(EncShape<D, P>::BT) k_encode_rows(EncArgs e, S
 }
 
 template <int D, int P, int M>
-static int encode_cells(int n, int64_t C, int nx, int wrapx, const PrecConsts& pc,
+static int encode_cells(int64_t C, int nx, int wrapx, const PrecConsts& pc,
                         const double* const x[3], const int32_t* items, const int32_t* start,
-                        void* pos_csr, int32_t* cell_slot, const SweepArgs& a, cudaStream_t st) {
-  (void)n;
-  (void)pos_csr;
-  (void)cell_slot;
+                        const SweepArgs& a, cudaStream_t st) {
   using E = EncShape<D, P>;
   EncArgs e;
   e.nx = nx;
@@ -1955,35 +1818,31 @@ static int encode_cells(int n, int64_t C, int nx, int wrapx, const PrecConsts& p
 template <int D, int P>
 static int encode_t(int mode, int n, int64_t C, int nx, int wrapx, const PrecConsts& pc,
                     const double* const x[3], const int32_t* items, const int32_t* start,
-                    void* pos_csr, int32_t* cell_slot, const SweepArgs& a, cudaStream_t st) {
+                    const SweepArgs& a, cudaStream_t st) {
   if (mode == MODE_ALL) {
-    k_encode_own<D, P, MODE_ALL><<<(n + 255) / 256, 256, 0, st>>>(n, x[0], x[1], x[2], nullptr,
-                                                                   nullptr, nullptr, a);
+    k_pack_own<D, P><<<(n + 255) / 256, 256, 0, st>>>(n, x[0], x[1], x[2],
+                                                       const_cast<void*>(a.pos_own));
     const int64_t nch = (n + 3) / 4;
     k_encode_all<D, P><<<(unsigned)((nch + 127) / 128), 128, 0, st>>>(n, a.pos_own, a);
     return 2;
   }
   if (C == 0) return 0;
-  if (mode == MODE_RCLL)
-    return encode_cells<D, P, MODE_RCLL>(n, C, nx, wrapx, pc, x, items, start, pos_csr, cell_slot, a, st);
-  return encode_cells<D, P, MODE_CLL>(n, C, nx, wrapx, pc, x, items, start, pos_csr, cell_slot, a, st);
+  if (mode == MODE_RCLL) return encode_cells<D, P, MODE_RCLL>(C, nx, wrapx, pc, x, items, start, a, st);
+  return encode_cells<D, P, MODE_CLL>(C, nx, wrapx, pc, x, items, start, a, st);
 }
 
 // Returns the number of kernel launches issued (n > 0).
 int launch_encode(int dim, int prec, int mode, int n, int64_t C, int nx, int wrapx,
                   const PrecConsts& pc, const double* const x[3], const int32_t* items,
-                  const int32_t* start, void* pos_csr, int32_t* cell_slot, const SweepArgs& a,
-                  cudaStream_t st) {
+                  const int32_t* start, const SweepArgs& a, cudaStream_t st) {
 #define ENC(D, P) \
-  if (dim == D && prec == P) return encode_t<D, P>(mode, n, C, nx, wrapx, pc, x, items, start, pos_csr, cell_slot, a, st);
+  if (dim == D && prec == P) return encode_t<D, P>(mode, n, C, nx, wrapx, pc, x, items, start, a, st);
   ENC(1, FP16) ENC(2, FP16) ENC(3, FP16) ENC(1, FP32) ENC(2, FP32) ENC(3, FP32)
   ENC(1, FP64) ENC(2, FP64) ENC(3, FP64)
 #undef ENC
   return 0;
 }
 
-// Returns the number of tile tickets the launch consumes (one per block, or one
-// per warp for k_rcll16); the caller advances its ticket base by exactly that.
 template <int D, int P, int M>
 static int64_t sweep_t(const SweepArgs& a, cudaStream_t st) {
   using S = Shape<D>;
