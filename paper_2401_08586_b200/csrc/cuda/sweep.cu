@@ -36,6 +36,10 @@
 #include <climits>
 #include <type_traits>
 
+#ifndef SPHX_TICKET
+#define SPHX_TICKET 0  // k_rcll16 tiles from blockIdx (1: from the ticket counter)
+#endif
+
 #include "common.cuh"
 
 namespace sphx_dev {
@@ -786,9 +790,15 @@ __global__ void __launch_bounds__(BT, R16Shape<D>::MINB) k_rcll16(SweepArgs a) {
   __shared__ int s_tile;
   __shared__ long long s_base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#if SPHX_TICKET
   if (tid == 0) s_tile = (int)(atomicAdd(a.ticket, 1ull) - a.tick0);
   __syncthreads();
   const int tile = s_tile;
+#else
+  // blocks are dispatched in index order, so tile = blockIdx.x never waits on a
+  // tile that has not started (a predecessor that never publishes traps)
+  const int tile = blockIdx.x;
+#endif
   const int r = tile * BT + tid;
   const bool valid = r < a.nrows;
   const int i = a.row0 + (valid ? r : 0);
@@ -1858,7 +1868,7 @@ static int64_t sweep_t(const SweepArgs& a, cudaStream_t st) {
     using R = R16Shape<D>;
     const int64_t nb = (a.nrows + R::BT - 1) / R::BT;
     k_rcll16<D, R::BT, R::PCAP, R::WMAX><<<(unsigned)nb, R::BT, 0, st>>>(a);
-    return nb;
+    return SPHX_TICKET ? nb : 0;  // tiles from blockIdx take no tickets
   } else {
     const int64_t nb = (a.nrows + S::BT - 1) / S::BT;
     k_sweep<D, P, M, S::BT, S::PCAP, S::WMAX><<<(unsigned)nb, S::BT, 0, st>>>(a);
