@@ -20,6 +20,11 @@
  *   sphx_rebuild_members <- void CellGrid::rebuild_members(const RelCoords&)
  *                                                                   cell_grid.hpp:150, cell_grid.cpp:86-108
  *   sphx_table_copy      <- (ownership hand-off of the returned NeighborTable, nnps.hpp:16-26)
+ *   sphx_update_relative(_device)
+ *                        <- void update_relative(RelCoords&, size_t i, const std::array<double,3>&,
+ *                                                const CellGrid&, Precision) for all i
+ *                                                                   cell_grid.hpp:134, cell_grid.cpp:180-212
+ *   sphx_rebuild_members_device <- CellGrid::rebuild_members on device memory
  *   sphx_rcll_grad_normalized(_device)
  *                        <- grad_normalized(f, ps, rcll(rc, grid, fp16), kp) fused
  *                                                                   gradient.cpp:44-82, dynamics.cpp:145-155
@@ -211,6 +216,27 @@ int sphx_rcll_distances_device(sphx_context* ctx, const sphx_grid_desc* grid, in
  * inputs); dist receives sphx_rcll's *total doubles (host memory, synchronous). */
 int sphx_table_distances(sphx_context* ctx, const sphx_grid_desc* grid, int32_t precision,
                          double* dist);
+
+/* RCLL maintenance: update_relative(rc, i, dx[i], grid, prec)
+ * (cell_grid.hpp:134, cell_grid.cpp:180-212) for every particle i < n at once --
+ * the Eq. 8 migration step_mixed applies after the drift (dynamics.cpp:191-198).
+ * Errors are the reference's std::runtime_error texts ("displacement skips a cell
+ * on axis k", "particle leaves the grid on axis k") for the lowest offending
+ * particle; rel/cell are then unspecified (the reference leaves them partially
+ * updated). Host memory, synchronous. */
+int sphx_update_relative(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                         double* const rel[3], int32_t* const cell[3], const double* const dx[3],
+                         int32_t precision);
+/* Device memory, stream-ordered: *d_status = ~0 on success, else
+ * (particle << 3) | (axis << 1) | kind (0: skips a cell, 1: leaves the grid). */
+int sphx_update_relative_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                                double* const d_rel[3], int32_t* const d_cell[3],
+                                const double* const d_dx[3], int32_t precision,
+                                unsigned long long* d_status);
+/* CellGrid::rebuild_members(rc) on device memory (cell_grid.cpp:86-108). */
+int sphx_rebuild_members_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                                const int32_t* const d_cell[3], int32_t* d_cell_of,
+                                int32_t* d_cell_start, int32_t* d_items);
 
 /* Fused FP16 RCLL -> grad_normalized: the mixed step's
  *   grad_normalized(f, ps, rcll(rel, grid, fp16), make_kernel(h, dim))

@@ -128,6 +128,7 @@ def _bind_ref(lib):
             "ref_table_hash": (C.c_uint64, [vp]),
             "ref_free_table": (None, [vp]),
             "ref_grad_normalized": (C.c_int64, [vp, vp, vp, C.c_double, vp, vp, vp]),
+            "ref_update_relative": (C.c_int64, [vp, vp, C.c_uint64, vp, vp, vp, C.c_int]),
             "ref_time_nnps": (C.c_double, [C.c_int, vp, vp, vp, C.c_int, C.c_int]),
         }
         for name, (res, args) in sig.items():
@@ -302,6 +303,13 @@ class RefSystem:
         return float(self.lib.ref_rel_distance(self.rel, self.grid, i, j, prec))
 
     # backends ----------------------------------------------------------------------
+    def update_relative(self, dx, prec):
+        """update_relative(rel, i, dx[:, i], grid, prec) for every particle in index
+        order (cell_grid.cpp:180-212); returns 0 or 1 + the particle that threw."""
+        dx = [np.ascontiguousarray(a, np.float64) for a in dx]
+        ptrs = [a.ctypes.data for a in dx] + [None] * (3 - len(dx))
+        return int(self.lib.ref_update_relative(self.rel, self.grid, self.n, *ptrs, prec))
+
     def grad_normalized_rcll(self, prec, f, h):
         """The reference's mixed step core: grad_normalized(f, ps, rcll(rel, grid, prec),
         make_kernel(h, dim)) (dynamics.cpp:145-155, gradient.cpp:44-82)."""
@@ -379,6 +387,8 @@ def _oracle_lib():
             "so_rel_distance": (C.c_double, [C.POINTER(SoGrid), C.POINTER(vp), C.POINTER(vp),
                                              C.c_int64, C.c_int64, C.c_int]),
             "so_table_free": (None, [C.POINTER(_SoTable)]),
+            "so_update_relative": (C.c_int64, [C.POINTER(SoGrid), C.c_int64, C.POINTER(vp),
+                                               C.POINTER(vp), C.POINTER(vp), C.c_int]),
             "so_grad_normalized": (C.c_int64, [C.c_int, C.c_int64, C.POINTER(vp), vp, vp, vp,
                                                C.c_double, C.POINTER(vp)]),
             "so_table_hash": (C.c_uint64, [C.POINTER(_SoTable)]),
@@ -487,6 +497,12 @@ class Oracle:
         if self.lib.so_all_list(len(xs), len(xs[0]), _ptrs(xs), h, prec, C.byref(t)) != 0:
             raise ValueError("all_list needs at least one particle")
         return _take_table(t)
+
+    def update_relative(self, g: SoGrid, rel, cell, dx, prec) -> int:
+        """In place on rel/cell (numpy); 0 or 1 + ((i << 3) | (axis << 1) | kind)."""
+        dx = [np.ascontiguousarray(a, np.float64) for a in dx]
+        return int(self.lib.so_update_relative(C.byref(g), len(rel[0]), _ptrs(rel), _ptrs(cell),
+                                               _ptrs(dx), prec))
 
     def grad_normalized(self, dim, x, f, offsets, items, h):
         """grad_normalized on a table (gradient.cpp:44-82): (g[dim], degenerate)."""

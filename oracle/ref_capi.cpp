@@ -286,6 +286,20 @@ void ref_table_copy(void* t, std::int64_t* offsets, std::int32_t* items) {
 std::uint64_t ref_table_hash(void* t) { return fnv_table(*static_cast<sphx::NeighborTable*>(t)); }
 void ref_free_table(void* t) { delete static_cast<sphx::NeighborTable*>(t); }
 
+// ---- update_relative over particles [0, n) (cell_grid.cpp:180-212) -----------------
+// 0, or 1 + the index of the particle whose update threw (message in ref_last_error).
+std::int64_t ref_update_relative(void* r, void* g, std::uint64_t n, const double* dx0,
+                                 const double* dx1, const double* dx2, int prec) {
+  auto& rc = *static_cast<sphx::RelCoords*>(r);
+  const auto& grid = *static_cast<sphx::CellGrid*>(g);
+  for (std::uint64_t i = 0; i < n; ++i) {
+    const std::array<double, 3> d{dx0 ? dx0[i] : 0.0, dx1 ? dx1[i] : 0.0, dx2 ? dx2[i] : 0.0};
+    if (guarded([&] { sphx::update_relative(rc, i, d, grid, prec_of(prec)); }) != 0)
+      return (std::int64_t)i + 1;
+  }
+  return 0;
+}
+
 // ---- gradient on a table (gradient.hpp:27, gradient.cpp:44-82) ------------------------
 std::int64_t ref_grad_normalized(void* ps, void* t, const double* f, double h, double* g0,
                                  double* g1, double* g2) {

@@ -659,3 +659,38 @@ int64_t so_grad_normalized(int dim, int64_t n, const double* const* x, const dou
   }
   return degenerate;
 }
+
+/* update_relative (cell_grid.cpp:180-212) for particles [0, n): returns 0, or
+ * 1 + ((i << 3) | (k << 1) | kind) for the first (particle, axis) that throws
+ * (kind 0: displacement skips a cell, 1: particle leaves the grid), with the
+ * particles before it updated, as the reference leaves them. */
+int64_t so_update_relative(const so_grid* g, int64_t n, double** rel, int32_t** cell,
+                           const double* const* dx, int prec) {
+  for (int64_t i = 0; i < n; ++i) {
+    for (int k = 0; k < g->dim; ++k) {
+      const double edge = g->edge[k];
+      if (!(fabs(dx[k][i]) < edge)) return 1 + ((i << 3) | ((int64_t)k << 1));
+      const double inc = so_round_to(prec, 2.0 * dx[k][i] / edge);
+      double r = so_round_to(prec, rel[k][i] + inc);
+      int32_t c = cell[k][i];
+      if (r > 1.0) {
+        r -= 2.0;
+        ++c;
+        if (c >= g->counts[k]) {
+          if (g->periodic[k]) c = 0;
+          else return 1 + ((i << 3) | ((int64_t)k << 1) | 1);
+        }
+      } else if (r < -1.0) {
+        r += 2.0;
+        --c;
+        if (c < 0) {
+          if (g->periodic[k]) c = g->counts[k] - 1;
+          else return 1 + ((i << 3) | ((int64_t)k << 1) | 1);
+        }
+      }
+      rel[k][i] = r;
+      cell[k][i] = c;
+    }
+  }
+  return 0;
+}

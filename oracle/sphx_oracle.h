@@ -90,6 +90,11 @@ int so_all_list(int dim, int64_t n, const double* const* x, double h, int prec, 
 double so_rel_distance(const so_grid* g, const double* const* rel, const int32_t* const* cell,
                        int64_t i, int64_t j, int prec);
 
+/* update_relative (cell_grid.cpp:180-212) over particles [0, n); 0 or
+ * 1 + ((i << 3) | (axis << 1) | kind) for the first throw. */
+int64_t so_update_relative(const so_grid* g, int64_t n, double** rel, int32_t** cell,
+                           const double* const* dx, int prec);
+
 /* grad_normalized (gradient.cpp:44-82) with the cubic B-spline gradient
  * (kernel.hpp:17-64): g[k][i] for every row of the table; returns the number of
  * degenerate (particle, axis) pairs. */

@@ -94,6 +94,9 @@ def lib():
                                           p3]),
         "sphx_rcll_distances_device": (C.c_int, [vp, G, i64, p3, p3, i32, vp, vp, vp]),
         "sphx_table_distances": (C.c_int, [vp, G, i32, vp]),
+        "sphx_update_relative": (C.c_int, [vp, G, i64, p3, p3, p3, i32]),
+        "sphx_update_relative_device": (C.c_int, [vp, G, i64, p3, p3, p3, i32, vp]),
+        "sphx_rebuild_members_device": (C.c_int, [vp, G, i64, p3, vp, vp, vp]),
         "sphx_rcll_grad_normalized": (C.c_int, [vp, G, i64, p3, p3, i64, vp, vp, i32, p3, vp, dbl,
                                                 p3, C.POINTER(i64)]),
         "sphx_rcll_grad_normalized_device": (C.c_int, [vp, G, i64, p3, p3, vp, vp, i32, p3, vp,
@@ -115,7 +118,8 @@ EXPORTED = ("sphx_last_error", "sphx_grid_init", "sphx_create", "sphx_destroy",
             "sphx_last_timing", "sphx_build_lattice", "sphx_build_random_uniform",
             "sphx_table_hash", "sphx_build_rel_coords_window_device", "sphx_rcll_rows_device",
             "sphx_lattice_device", "sphx_rcll_distances_device", "sphx_table_distances",
-            "sphx_rcll_grad_normalized", "sphx_rcll_grad_normalized_device")
+            "sphx_rcll_grad_normalized", "sphx_rcll_grad_normalized_device",
+            "sphx_update_relative", "sphx_update_relative_device", "sphx_rebuild_members_device")
 
 
 def table_hash(offsets: np.ndarray, items: np.ndarray) -> int:
@@ -258,6 +262,26 @@ class Context:
                               items.ctypes.data, cell_start.ctypes.data, prec, C.byref(tot)))
         self._last_total = tot.value
         return self._fetch(n, tot.value)
+
+    def update_relative(self, grid: GridDesc, rel, cell, dx, prec: int):
+        """update_relative for every particle (host arrays are updated in place)."""
+        for a in list(rel) + list(cell):
+            assert a.flags["C_CONTIGUOUS"]
+        dx = [_c64(a) for a in dx]
+        check(lib().sphx_update_relative(self.h, C.byref(grid), len(rel[0]), _ptr3(rel),
+                                         _ptr3(cell), _ptr3(dx), prec))
+
+    def update_relative_device(self, grid, rel, cell, dx, prec, status):
+        self._bind(status)
+        check(lib().sphx_update_relative_device(self.h, C.byref(grid), rel[0].numel(), _dptr3(rel),
+                                                _dptr3(cell), _dptr3(dx), prec,
+                                                status.data_ptr()))
+
+    def rebuild_members_device(self, grid, cell, cell_of, cell_start, items):
+        self._bind(items)
+        check(lib().sphx_rebuild_members_device(self.h, C.byref(grid), cell[0].numel(),
+                                                _dptr3(cell), cell_of.data_ptr(),
+                                                cell_start.data_ptr(), items.data_ptr()))
 
     def rcll_grad_normalized(self, grid: GridDesc, rel, cell, items, cell_start, prec: int, x, f,
                              h: float):

@@ -34,6 +34,10 @@ void launch_scan_counts(const int32_t* in, int32_t* out, int64_t C, unsigned lon
 void launch_scatter_sort(int n, int64_t C, const int32_t* cell_of, const int32_t* slot,
                          const int32_t* start, int32_t* items, cudaStream_t st);
 int launch_rcll_grad(int dim, const SweepArgs& a, cudaStream_t st);
+int launch_update_relative(int64_t n, int dim, int prec, double* const rel[3],
+                           int32_t* const cell[3], const double* const dx[3],
+                           const double edge[3], const int counts[3], const int periodic[3],
+                           unsigned long long* status, cudaStream_t st);
 int launch_rcll_distances(int dim, int prec, int64_t nrows, const GridConsts& g,
                           const PrecConsts& pc, const double hc[3], const double* const rel[3],
                           const int32_t* const cell[3], const int64_t* off,
@@ -808,6 +812,84 @@ int sphx_rebin_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
   CK(cudaMemsetAsync(d_bad, 0xFF, sizeof(int64_t), ctx->stream));
   return run_binning(ctx, 0, *grid, n, d_x, nullptr, nullptr, nullptr, d_cell_of, d_cell_start,
                      d_items, reinterpret_cast<unsigned long long*>(d_bad));
+}
+
+// ---------------- RCLL maintenance (update_relative + rebuild_members) ----------------
+
+int sphx_update_relative_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                                double* const d_rel[3], int32_t* const d_cell[3],
+                                const double* const d_dx[3], int32_t precision,
+                                unsigned long long* d_status) {
+  TRY(check_ctx(ctx));
+  if (!grid || !d_status) return fail(SPHX_ERR_INVALID_ARGUMENT, "null argument");
+  TRY(check_prec_dim(precision, grid->dim));
+  double edge[3] = {0.0, 0.0, 0.0};
+  int counts[3] = {1, 1, 1}, periodic[3] = {0, 0, 0};
+  double* rel[3] = {nullptr, nullptr, nullptr};
+  int32_t* cell[3] = {nullptr, nullptr, nullptr};
+  const double* dx[3] = {nullptr, nullptr, nullptr};
+  for (int k = 0; k < grid->dim; ++k) {
+    // CellGrid::edge_phys (cell_grid.cpp:9-34): span / count on a periodic axis, else 2h
+    edge[k] = grid->periodic[k] ? (grid->hi[k] - grid->lo[k]) / grid->counts[k] : grid->radius_phys;
+    counts[k] = grid->counts[k];
+    periodic[k] = grid->periodic[k] != 0;
+    rel[k] = d_rel[k];
+    cell[k] = d_cell[k];
+    dx[k] = d_dx[k];
+  }
+  CK(cudaMemsetAsync(d_status, 0xFF, sizeof(unsigned long long), ctx->stream));
+  ctx->launches += launch_update_relative(n, grid->dim, precision, rel, cell, dx, edge, counts,
+                                          periodic, d_status, ctx->stream);
+  CKL();
+  return SPHX_OK;
+}
+
+int sphx_update_relative(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                         double* const rel[3], int32_t* const cell[3], const double* const dx[3],
+                         int32_t precision) {
+  TRY(check_ctx(ctx));
+  if (!grid) return fail(SPHX_ERR_INVALID_ARGUMENT, "null grid");
+  TRY(check_prec_dim(precision, grid->dim));
+  const int dim = grid->dim;
+  double* d_rel[3] = {nullptr, nullptr, nullptr};
+  int32_t* d_cell[3] = {nullptr, nullptr, nullptr};
+  const double* d_dx[3] = {nullptr, nullptr, nullptr};
+  for (int k = 0; k < dim; ++k) {
+    TRY(upload(ctx, ctx->b_rel[k], rel[k], sizeof(double) * n));
+    TRY(upload(ctx, ctx->b_cell[k], cell[k], sizeof(int32_t) * n));
+    TRY(upload(ctx, ctx->g_x[k], dx[k], sizeof(double) * n));
+    d_rel[k] = ctx->b_rel[k].as<double>();
+    d_cell[k] = ctx->b_cell[k].as<int32_t>();
+    d_dx[k] = ctx->g_x[k].as<double>();
+  }
+  TRY(ctx->b_bad.ensure(sizeof(unsigned long long)));
+  TRY(sphx_update_relative_device(ctx, grid, n, d_rel, d_cell, d_dx, precision,
+                                  ctx->b_bad.as<unsigned long long>()));
+  unsigned long long st = ~0ull;
+  CK(cudaMemcpyAsync(&st, ctx->b_bad.p, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream));
+  for (int k = 0; k < dim && n; ++k) {
+    CK(cudaMemcpyAsync(rel[k], d_rel[k], sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(cell[k], d_cell[k], sizeof(int32_t) * n, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (st != ~0ull) {  // the message std::runtime_error carries (cell_grid.cpp:185, 196, 205)
+    const int axis = (int)((st >> 1) & 3);
+    return fail(SPHX_ERR_RUNTIME, (st & 1) ? "particle leaves the grid on axis " + std::to_string(axis)
+                                           : "displacement skips a cell on axis " + std::to_string(axis));
+  }
+  return SPHX_OK;
+}
+
+int sphx_rebuild_members_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t n,
+                                const int32_t* const d_cell[3], int32_t* d_cell_of,
+                                int32_t* d_cell_start, int32_t* d_items) {
+  TRY(check_ctx(ctx));
+  if (!grid) return fail(SPHX_ERR_INVALID_ARGUMENT, "null grid");
+  TRY(check_prec_dim(SPHX_FP64, grid->dim));
+  TRY(ctx->b_bad.ensure(sizeof(unsigned long long)));
+  return run_binning(ctx, 2, *grid, n, nullptr, d_cell, nullptr, nullptr, d_cell_of, d_cell_start,
+                     d_items, ctx->b_bad.as<unsigned long long>());
 }
 
 // ---------------- multi-GPU slab path ----------------

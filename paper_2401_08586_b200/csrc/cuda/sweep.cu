@@ -36,6 +36,12 @@
 #include <climits>
 #include <type_traits>
 
+#ifndef SPHX_UNROLL
+#define SPHX_UNROLL 4
+#endif
+#ifndef SPHX_MINB2
+#define SPHX_MINB2 12
+#endif
 #ifndef SPHX_TICKET
 #define SPHX_TICKET 0  // k_rcll16 tiles from blockIdx (1: from the ticket counter)
 #endif
@@ -43,6 +49,8 @@
 #include "common.cuh"
 
 namespace sphx_dev {
+
+constexpr int kPhaseAUnroll = SPHX_UNROLL;  // chunk loads issued together in phase A
 
 // ------------------------------------------------------------------------------
 // Own-particle coordinates (particle order): FP16 half2 / half4, FP32/FP64 vectors.
@@ -777,7 +785,7 @@ struct R16Shape {
   static constexpr int BT = D == 3 ? 64 : 128;
   static constexpr int PCAP = D == 3 ? 64 * 60 : 128 * 20;  // packed rows per tile
   static constexpr int WMAX = D == 3 ? 20 : 4;              // hit words kept per row
-  static constexpr int MINB = D == 3 ? 14 : 12;             // CTAs per SM (register budget)
+  static constexpr int MINB = D == 3 ? 14 : SPHX_MINB2;     // CTAs per SM (register budget)
 };
 
 template <int D, int BT, int PCAP, int WMAX>
@@ -787,10 +795,10 @@ __global__ void __launch_bounds__(BT, R16Shape<D>::MINB) k_rcll16(SweepArgs a) {
   __shared__ unsigned NIB[WMAX * BT];
   __shared__ int2 RUNS[NR * BT];
   __shared__ int s_w[BT / 32];
-  __shared__ int s_tile;
   __shared__ long long s_base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #if SPHX_TICKET
+  __shared__ int s_tile;
   if (tid == 0) s_tile = (int)(atomicAdd(a.ticket, 1ull) - a.tick0);
   __syncthreads();
   const int tile = s_tile;
@@ -858,7 +866,7 @@ __global__ void __launch_bounds__(BT, R16Shape<D>::MINB) k_rcll16(SweepArgs a) {
     for (int g = c.ch; g < c.end; g += 8) {
       const int e = min(g + 8, c.end);
       unsigned acc = 0;
-#pragma unroll 4
+#pragma unroll(kPhaseAUnroll)
       for (int ch = g; ch < e; ++ch) {
         r16_chunk<D>(qc, ch, r2, hh2, hc2, thr2, c.ccy, c.ccz, acc);
         if (ch == selfch) acc &= selfmask;

@@ -184,3 +184,27 @@ def test_oracle_grad_normalized_matches_reference(dim, ds, jitter):
         assert dr == do
         for a, b in zip(gr, go):
             assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("prec", [0, 1, 2])
+@pytest.mark.parametrize("periodic", [(0, 0, 0), (1, 1, 0)])
+def test_oracle_update_relative_matches_reference(prec, periodic):
+    """so_update_relative == the reference's update_relative, including where it
+    throws (the particles before the throw updated, the rest untouched)."""
+    if not os.path.exists(O.REF_SO):
+        pytest.skip("reference library not built")
+    ds = 0.02
+    r = O.RefSystem.lattice(2, ds, 0.3, 1).make_grid(periodic=tuple(bool(p) for p in periodic))
+    orc = O.Oracle()
+    og = orc.grid(2, 2.4 * ds, periodic=periodic)
+    rel, cell = [np.array(a) for a in r.rel_coords()[0]], [np.array(a) for a in r.rel_coords()[1]]
+    rng = np.random.default_rng(11)
+    dx = [rng.uniform(-0.45, 0.45, r.n) * og.edge[k] for k in range(2)]
+    e_ref = r.update_relative(dx, prec)
+    e_or = orc.update_relative(og, rel, cell, dx, prec)
+    assert (e_ref == 0) == (e_or == 0)
+    if e_ref:
+        assert e_ref - 1 == (e_or - 1) >> 3
+    rr, rc = r.rel_coords()
+    for k in range(2):
+        assert np.array_equal(rr[k], rel[k]) and np.array_equal(rc[k], cell[k])
