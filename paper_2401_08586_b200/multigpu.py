@@ -476,7 +476,7 @@ def bench(args, workloads, metric, clock_sampler=None, peaks=(6650.0, "fallback"
                        "l2": "flushed between timed steps (256 MiB write, outside the events)"},
             "pipeline": {"ms_per_step": t_pipe * 1e3, "value": owned / t_pipe,
                          "what": "halo exchange (NCCL p2p) + window binning + rows"},
-            "roofline": {"bound": "hbm", "kernel": "k_count + k_fill (rank 0)",
+            "roofline": {"bound": "hbm", "kernel": "k_rcll16 (2-D) / k_r16_test + k_r16_emit (3-D), rank 0",
                          "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": None,
                          "algorithmic_bytes": b_sweep},
