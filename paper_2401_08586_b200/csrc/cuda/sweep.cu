@@ -914,9 +914,11 @@ __global__ void __launch_bounds__(BT, R16Shape<D>::MINB) k_rcll16(SweepArgs a) {
           word >>= 4 * (8 - (e - g));
         }
         ++wq;
-        for (int ch = g; word; ++ch, word >>= 4) {
-          const unsigned m = word & 15u;
-          if (m) append4(dst, kk, m, __ldg(tags + ch));
+        while (word) {  // next chunk with hits
+          const int sh = (__ffs(word) - 1) & ~3;
+          const unsigned m = (word >> sh) & 15u;
+          word &= ~(15u << sh);
+          append4(dst, kk, m, __ldg(tags + g + (sh >> 2)));
         }
       }
       if (gs > 0 && kk > gs && dst.ld(gs) < dst.ld(gs - 1)) merge_tail(dst, gs, kk);
@@ -1112,9 +1114,11 @@ __global__ void __launch_bounds__(BT, R16Two<D>::EMINB) k_r16_emit(SweepArgs a) 
         unsigned word = w < W ? __ldg(a.hitw + (int64_t)w * a.nrows + r)
                               : own.template group<Q>(qc, g, min(g + 8, ce[Q]));
         ++w;
-        for (int ch = g; word; ++ch, word >>= 4) {
-          const unsigned m = word & 15u;
-          if (m) append4(dst, kk, m, __ldg(tags + ch));
+        while (word) {  // next chunk with hits
+          const int sh = (__ffs(word) - 1) & ~3;
+          const unsigned m = (word >> sh) & 15u;
+          word &= ~(15u << sh);
+          append4(dst, kk, m, __ldg(tags + g + (sh >> 2)));
         }
       }
       if (gs > 0 && kk > gs && dst.ld(gs) < dst.ld(gs - 1)) merge_tail(dst, gs, kk);
@@ -1245,9 +1249,11 @@ __global__ void __launch_bounds__(BT) k_r16_grad(SweepArgs a) {
         for (int g = cb[Q]; g < ce[Q]; g += 8) {
           unsigned word = word_at(wq, qv, g);
           ++wq;
-          for (int ch = g; word; ++ch, word >>= 4) {
-            const unsigned m = word & 15u;
-            if (m) append4(row, kk, m, __ldg(tags + ch));
+          while (word) {  // next chunk with hits
+            const int sh = (__ffs(word) - 1) & ~3;
+            const unsigned m = (word >> sh) & 15u;
+            word &= ~(15u << sh);
+            append4(row, kk, m, __ldg(tags + g + (sh >> 2)));
           }
         }
         if (gs > 0 && kk > gs && row.ld(gs) < row.ld(gs - 1)) merge_tail(row, gs, kk);
@@ -1374,9 +1380,11 @@ __global__ void __launch_bounds__(BT) k_sweep(SweepArgs a) {
                                : group_word<D, P, MODE>(a, tst, row, own, selfch, selfmask, g, e);
       ++w;
       const int gs = kk;
-      for (int ch = g; word; ++ch, word >>= 4) {
-        const unsigned m = word & 15u;
-        if (m) append4(dst, kk, m, __ldg(tags + ch));
+      while (word) {  // next chunk with hits
+        const int sh = (__ffs(word) - 1) & ~3;
+        const unsigned m = (word >> sh) & 15u;
+        word &= ~(15u << sh);
+        append4(dst, kk, m, __ldg(tags + g + (sh >> 2)));
       }
       if (gs > 0 && kk > gs && dst.ld(gs) < dst.ld(gs - 1)) merge_tail(dst, gs, kk);
     });
