@@ -1711,9 +1711,11 @@ __global__ void __launch_bounds__(EncShape<D, P>::BT) k_encode_rows(EncArgs e, S
   // number of keys < key in window cell u
   auto less_in = [&](int u, int key) {
     int lo = wst[u], hi = wst[u + 1];
-    if (win_sm && hi - lo <= 16) {
+    if (win_sm && hi - lo <= 16) {  // branch-free for the first 8 keys
       int c = 0;
-      for (int q = lo; q < hi; ++q) c += skey[q] < key;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) c += (lo + q < hi) & (skey[min(lo + q, hi - 1)] < key);
+      for (int q = lo + 8; q < hi; ++q) c += skey[q] < key;
       return c;
     }
     while (lo < hi) {
