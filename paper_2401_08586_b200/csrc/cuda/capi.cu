@@ -23,7 +23,7 @@ int launch_encode(int dim, int prec, int mode, int n, int64_t C, int nx, int wra
 int64_t launch_sweep(int dim, int prec, int mode, const SweepArgs& a, cudaStream_t st);
 size_t coord_bytes(int dim, int prec);
 size_t chunk_bytes(int dim, int prec, int mode);
-int64_t chunk_capacity(int mode, int64_t n, int64_t C);
+int64_t chunk_capacity(int dim, int prec, int mode, int64_t n, int64_t C);
 int sweep_tile(int dim, int prec, int mode);
 int hit_words(int dim, int prec, int mode);
 // binning.cu
@@ -125,7 +125,7 @@ struct sphx_context {
   // inputs staged from host
   Buf in_x[3], in_cell[3], in_items, in_start, in_cellof;
   // encode / sweep scratch
-  Buf pos_own, tri, qc, qtag, selfpos;
+  Buf pos_own, tri, qc, qtag, selfpos, xy_nch, xy_cstart, xy_tiles;
   // single-pass sweep: look-back words (epoch-tagged) and the tile ticket
   Buf sw_tiles, sw_ticket, sw_rowk, sw_hitw;
   unsigned long long sw_tick = 0;
@@ -321,12 +321,17 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
     return SPHX_OK;
   }
   const int64_t C = mode == MODE_ALL ? 0 : cell_total(g);
-  const int64_t chunks = chunk_capacity(mode, n, C);
+  const int64_t chunks = chunk_capacity(g.dim, prec, mode, n, C);
   TRY(ctx->pos_own.ensure(coord_bytes(g.dim, prec) * (size_t)n));
   TRY(ctx->qc.ensure(chunk_bytes(g.dim, prec, mode) * (size_t)chunks));
   TRY(ctx->qtag.ensure(16 * (size_t)chunks));
   if (mode != MODE_ALL) {
     TRY(ctx->tri.ensure(sizeof(int2) * std::max<int64_t>(C, 1)));
+    if (g.dim == 3 && prec == SPHX_FP16 && mode == MODE_RCLL) {  // xy-plane runs
+      TRY(ctx->xy_nch.ensure(sizeof(int32_t) * std::max<int64_t>(C, 1)));
+      TRY(ctx->xy_cstart.ensure(sizeof(int32_t) * (C + 1)));
+      TRY(ctx->xy_tiles.ensure(sizeof(unsigned long long) * (scan_tiles(C) + 2)));
+    }
     TRY(ctx->selfpos.ensure(sizeof(int32_t) * (size_t)n));
   }
 
@@ -338,6 +343,9 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
   a.nchunks = chunks;
   a.qtag = ctx->qtag.p;
   a.selfpos = ctx->selfpos.as<int32_t>();
+  a.xy_nch = ctx->xy_nch.as<int32_t>();
+  a.xy_cstart = ctx->xy_cstart.as<int32_t>();
+  a.xy_tiles = ctx->xy_tiles.as<unsigned long long>();
   a.pos_own = ctx->pos_own.p;
   for (int k = 0; k < 3; ++k) a.cellk[k] = cellk ? cellk[k] : nullptr;
   a.cell_of = cell_of;
@@ -565,7 +573,7 @@ void sphx_destroy(sphx_context* ctx) {
   cudaStreamSynchronize(ctx->stream);
   Buf* all[] = {&ctx->in_x[0], &ctx->in_x[1], &ctx->in_x[2], &ctx->in_cell[0], &ctx->in_cell[1],
                 &ctx->in_cell[2], &ctx->in_items, &ctx->in_start, &ctx->in_cellof, &ctx->pos_own,
-                &ctx->tri, &ctx->qc,
+                &ctx->tri, &ctx->qc, &ctx->xy_nch, &ctx->xy_cstart, &ctx->xy_tiles,
                 &ctx->qtag, &ctx->selfpos, &ctx->sw_tiles, &ctx->sw_ticket, &ctx->sw_rowk, &ctx->sw_hitw, &ctx->t_offsets, &ctx->t_items, &ctx->t_dist, &ctx->g_x[0], &ctx->g_x[1], &ctx->g_x[2],
                 &ctx->g_f, &ctx->g_out[0], &ctx->g_out[1], &ctx->g_out[2], &ctx->g_deg,
                 &ctx->b_counts, &ctx->b_slot, &ctx->b_bad, &ctx->b_tiles, &ctx->b_out_cellof,

@@ -62,6 +62,9 @@ struct SweepArgs {
   unsigned long long* ticket; // tile ticket counter (monotone across calls)
   unsigned long long tick0;   // ticket value at this call's first tile
   unsigned epoch;             // this call's look-back epoch (1..65535)
+  int32_t* xy_nch;            // 3-D FP16 RCLL encode: [C] chunks per xy run
+  int32_t* xy_cstart;         //   [C+1] first chunk of each run (scan of xy_nch)
+  unsigned long long* xy_tiles;  // scan look-back words + counter (zeroed per call)
   int32_t* rowk;              // [nrows] row lengths of the test pass (bit 31: words overflowed)
   unsigned* hitw;             // [W][nrows] hit words of the test pass
 };

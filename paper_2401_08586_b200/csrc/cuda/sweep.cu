@@ -50,6 +50,11 @@
 
 namespace sphx_dev {
 
+// binning.cu
+int64_t scan_tiles(int64_t C);
+void launch_scan_counts(const int32_t* in, int32_t* out, int64_t C, unsigned long long* tiles,
+                        int* counter, cudaStream_t st);
+
 constexpr int kPhaseAUnroll = SPHX_UNROLL;  // chunk loads issued together in phase A
 
 // ------------------------------------------------------------------------------
@@ -223,6 +228,12 @@ struct ChunkLay {
   static constexpr int NQ = D + (MODE == MODE_RCLL ? 1 : 0);
   static constexpr int NQP = NQ <= 1 ? 1 : (NQ <= 2 ? 2 : 4);
   static constexpr int BYTES = QB * NQP;
+};
+// 3-D FP16 RCLL uses xy-plane runs (k_encode_xy): records {x, y, z, dcx, dcy}
+// quads, 40 bytes padded to 48 (three 16-byte loads).
+template <>
+struct ChunkLay<3, FP16, MODE_RCLL> {
+  static constexpr int QB = 8, NQ = 5, NQP = 6, BYTES = 48;
 };
 
 // element u (0..3) of quad q of chunk ch
@@ -709,7 +720,9 @@ __device__ __forceinline__ long long lookback_resolve(unsigned long long* tiles,
 // ------------------------------------------------------------------------------
 template <int D>
 struct R16 {
-  static constexpr int NR = D == 3 ? 9 : 3;  // runs per particle
+  // runs per particle: 2-D x-triples of rows dy = -1, 0, 1; 3-D xy-plane runs of
+  // planes dz = -1, 0, 1 (k_encode_xy)
+  static constexpr int NR = 3;
 };
 
 // One chunk (4 candidates) against particle i: the 4-bit hit nibble is shifted
@@ -718,32 +731,41 @@ template <int D>
 __device__ __forceinline__ void r16_chunk(const char* __restrict__ qc, int ch, const __half2 (&r2)[3],
                                           const __half2 (&hh2)[3], __half2 hc2, __half2 thr2,
                                           __half2 ccy, __half2 ccz, unsigned& acc) {
-  const uint4* p = reinterpret_cast<const uint4*>(qc + (size_t)ch * 32);
-  const uint4 v0 = __ldg(p);
-  uint4 v1;
-  if constexpr (D == 3) {
-    v1 = __ldg(p + 1);
-  } else {
-    const uint2 t = __ldg(reinterpret_cast<const uint2*>(p + 1));
-    v1 = make_uint4(t.x, t.y, 0u, 0u);
-  }
-  // quads: x = (v0.x, v0.y), y = (v0.z, v0.w), 3-D z = (v1.x, v1.y), dc = last quad
-  const unsigned dcl = D == 3 ? v1.z : v1.x, dch = D == 3 ? v1.w : v1.y;
   __half2 a[2];
+  if constexpr (D == 3) {
+    // xy-plane run record (48 B): x, y quads | z, dcx quads | dcy quad; ccy is the
+    // y cell edge (dcy per record), ccz the run's z centre difference
+    const uint4* p = reinterpret_cast<const uint4*>(qc + (size_t)ch * 48);
+    const uint4 v0 = __ldg(p), v1 = __ldg(p + 1);
+    const uint2 v2 = __ldg(reinterpret_cast<const uint2*>(p + 2));
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const unsigned xj = h ? v0.y : v0.x, yj = h ? v0.w : v0.z;
-    __half2 t = __hmul2_rn(__hsub2_rn(r2[0], u2h(xj)), hh2[0]);
-    const __half2 d = __hfma2(u2h(h ? dch : dcl), hc2, t);
-    __half2 acc2 = __hmul2_rn(d, d);
-    t = __hadd2_rn(__hmul2_rn(__hsub2_rn(r2[1], u2h(yj)), hh2[1]), ccy);
-    acc2 = __hadd2_rn(acc2, __hmul2_rn(t, t));
-    if constexpr (D == 3) {
-      const unsigned zj = h ? v1.y : v1.x;
+    for (int h = 0; h < 2; ++h) {
+      const unsigned xj = h ? v0.y : v0.x, yj = h ? v0.w : v0.z, zj = h ? v1.y : v1.x;
+      __half2 t = __hmul2_rn(__hsub2_rn(r2[0], u2h(xj)), hh2[0]);
+      __half2 d = __hfma2(u2h(h ? v1.w : v1.z), hc2, t);
+      __half2 acc2 = __hmul2_rn(d, d);
+      t = __hmul2_rn(__hsub2_rn(r2[1], u2h(yj)), hh2[1]);
+      d = __hfma2(u2h(h ? v2.y : v2.x), ccy, t);
+      acc2 = __hadd2_rn(acc2, __hmul2_rn(d, d));
       t = __hadd2_rn(__hmul2_rn(__hsub2_rn(r2[2], u2h(zj)), hh2[2]), ccz);
       acc2 = __hadd2_rn(acc2, __hmul2_rn(t, t));
+      a[h] = acc2;
     }
-    a[h] = acc2;
+  } else {
+    const uint4* p = reinterpret_cast<const uint4*>(qc + (size_t)ch * 32);
+    const uint4 v0 = __ldg(p);
+    const uint2 v1 = __ldg(reinterpret_cast<const uint2*>(p + 1));
+    // quads: x = (v0.x, v0.y), y = (v0.z, v0.w), dc = (v1.x, v1.y)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const unsigned xj = h ? v0.y : v0.x, yj = h ? v0.w : v0.z;
+      __half2 t = __hmul2_rn(__hsub2_rn(r2[0], u2h(xj)), hh2[0]);
+      const __half2 d = __hfma2(u2h(h ? v1.y : v1.x), hc2, t);
+      __half2 acc2 = __hmul2_rn(d, d);
+      t = __hadd2_rn(__hmul2_rn(__hsub2_rn(r2[1], u2h(yj)), hh2[1]), ccy);
+      acc2 = __hadd2_rn(acc2, __hmul2_rn(t, t));
+      a[h] = acc2;
+    }
   }
   acc_nibble(acc, a[0], a[1], thr2);
 }
@@ -976,12 +998,13 @@ __device__ __forceinline__ void r16_runs(const SweepArgs& a, int i, bool valid, 
   const bool ok = valid && cx >= 0 && cx < nx && cy >= 0 && cy < ny && cz >= 0 && cz < nz;
 #pragma unroll
   for (int q = 0; q < NR; ++q) {
-    const int dy = (q % 3) - 1, dz = D == 3 ? (q / 3) - 1 : 0;
-    int y = cy + dy, z = cz + dz;
+    // 2-D: the x-triple of row cy + q - 1; 3-D: the xy run of plane cz + q - 1
+    int y = D == 3 ? cy : cy + q - 1, z = D == 3 ? cz + q - 1 : 0;
     bool in = ok;
-    if (y < 0) { y += ny; in = in && a.g.wrap[1]; }
-    else if (y >= ny) { y -= ny; in = in && a.g.wrap[1]; }
-    if (D == 3) {
+    if (D == 2) {
+      if (y < 0) { y += ny; in = in && a.g.wrap[1]; }
+      else if (y >= ny) { y -= ny; in = in && a.g.wrap[1]; }
+    } else {
       if (z < 0) { z += nz; in = in && a.g.wrap[2]; }
       else if (z >= nz) { z -= nz; in = in && a.g.wrap[2]; }
     }
@@ -1017,8 +1040,10 @@ struct R16Own {
   // hit word of chunks [g, e) of the run in slot q
   template <int Q>
   __device__ __forceinline__ unsigned group(const char* __restrict__ qc, int g, int e) const {
-    constexpr int dy = (Q % 3) - 1, dz = D == 3 ? (Q / 3) - 1 : 0;
-    const __half2 ccy = cc_of(hcy, dy), ccz = cc_of(hcz, dz);
+    // 2-D: the run's y centre difference; 3-D: per-record dcy times the y edge,
+    // and the run's z centre difference
+    const __half2 ccy = D == 3 ? __half2half2(hbits(hcy)) : cc_of(hcy, Q - 1);
+    const __half2 ccz = D == 3 ? cc_of(hcz, Q - 1) : u2h(0u);
     unsigned acc = 0;
 #pragma unroll 4
     for (int ch = g; ch < e; ++ch) {
@@ -1526,8 +1551,10 @@ size_t chunk_bytes(int dim, int prec, int mode) {
   return 0;
 }
 // chunks the candidate arrays need
-int64_t chunk_capacity(int mode, int64_t n, int64_t C) {
-  return mode == MODE_ALL ? (n + 3) / 4 + 1 : (3 * n + 6 * C) / 4 + 2;
+int64_t chunk_capacity(int dim, int prec, int mode, int64_t n, int64_t C) {
+  if (mode == MODE_ALL) return (n + 3) / 4 + 1;
+  if (dim == 3 && prec == FP16 && mode == MODE_RCLL) return (9 * n) / 4 + C + 2;  // xy runs
+  return (3 * n + 6 * C) / 4 + 2;
 }
 
 // ------------------------------------------------------------------------------
@@ -1548,6 +1575,8 @@ int64_t chunk_capacity(int mode, int64_t n, int64_t C) {
 // ------------------------------------------------------------------------------
 struct EncArgs {
   int nx, nxb, wrapx;
+  int ny, wrapy;               // xy-plane runs (3-D FP16 RCLL)
+  const int32_t* cstart;       // xy runs: first chunk of each cell's run (scan), [C+1]
   int64_t nrows;               // cell rows (ny * nz)
   const int32_t* start;        // CellGrid::cell_start
   const int32_t* items;        // CellGrid::items
@@ -1822,6 +1851,261 @@ __global__ void __launch_bounds__(EncShape<D, P>::BT) k_encode_rows(EncArgs e, S
   }
 }
 
+// ------------------------------------------------------------------------------
+// 3-D FP16 RCLL: xy-plane runs. The run of cell (x, y, z) is the id-merge of the
+// nine cells (x-1..x+1, y-1..y+1, z) (wrapped on periodic x / y, absent beyond a
+// wall); each record carries dcx and dcy (= -offset, the minimum image, nnps.cpp:
+// 359-362). A particle then has 3 runs (dz = -1, 0, 1) whose hits interleave only
+// where a lattice plane straddles two cell planes, so its row is built with few
+// merges. Run slots are a scan of the run lengths (k_xy_runlen + k_scan_counts).
+// ------------------------------------------------------------------------------
+__global__ void k_xy_runlen(int64_t C, int nx, int ny, int wrapx, int wrapy,
+                            const int32_t* __restrict__ start, int32_t* __restrict__ nch) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const int x = (int)(c % nx), y = (int)((c / nx) % ny);
+  const int64_t plane = c - x - (int64_t)y * nx;
+  int len = 0;
+#pragma unroll
+  for (int dy = -1; dy <= 1; ++dy) {
+    int yy = y + dy;
+    if (yy < 0 || yy >= ny) {
+      if (!wrapy) continue;
+      yy = yy < 0 ? yy + ny : yy - ny;
+    }
+#pragma unroll
+    for (int dx = -1; dx <= 1; ++dx) {
+      int xx = x + dx;
+      if (xx < 0 || xx >= nx) {
+        if (!wrapx) continue;
+        xx = xx < 0 ? xx + nx : xx - nx;
+      }
+      const int64_t cc = plane + (int64_t)yy * nx + xx;
+      len += __ldg(start + cc + 1) - __ldg(start + cc);
+    }
+  }
+  nch[c] = (len + 3) >> 2;
+}
+
+struct XYShape {
+  static constexpr int XB = 16, BT = 256;
+  static constexpr int NW = XB + 4;      // window cells per row (x0-2 .. x1+1)
+  static constexpr int WCAP = 1024;      // staged window members
+  static constexpr int OCAP = 640;       // staged chunks (48 B + 16 B ids each)
+};
+
+constexpr size_t xy_smem_bytes() {
+  return (size_t)XYShape::WCAP * (4 + 4 + 3 * 2) + (size_t)XYShape::OCAP * (48 + 16);
+}
+
+__global__ void __launch_bounds__(XYShape::BT) k_encode_xy(EncArgs e, SweepArgs a) {
+  using S = XYShape;
+  using L = ChunkLay<3, FP16, MODE_RCLL>;
+  constexpr int XB = S::XB, BT = S::BT, NW = S::NW, NWC = 3 * NW;
+  extern __shared__ __align__(16) unsigned char sm[];
+  int32_t* skey = reinterpret_cast<int32_t*>(sm);
+  int32_t* sid = skey + S::WCAP;
+  __half* scrd = reinterpret_cast<__half*>(sid + S::WCAP);  // [3][WCAP]
+  unsigned char* sch = sm + (size_t)S::WCAP * 14;            // [OCAP][48]
+  uint32_t* stag = reinterpret_cast<uint32_t*>(sch + (size_t)S::OCAP * L::BYTES);
+  __shared__ int wst[NWC + 1];   // window member offset of window cell w = r * NW + u
+  __shared__ int wgs[NWC];       // CSR slot of window cell w's first member
+  __shared__ int64_t s_ch0;
+  __shared__ int s_nch;
+
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int nx = e.nx, ny = e.ny;
+  const int64_t row = blockIdx.x / e.nxb;        // (y, z) row of the centre cells
+  const int x0 = (int)(blockIdx.x % e.nxb) * XB;
+  const int x1 = min(x0 + XB, nx);
+  const int y = (int)(row % ny);
+  const int64_t plane = (row - y) * nx;         // first cell of plane z
+  const int nrun = x1 - x0;
+
+  // window cells: rows y-1, y, y+1 (r = 0, 1, 2), columns x0-2 .. x1+1
+  if (tid < 32) {
+    int tot = 0;
+    for (int w0 = 0; w0 < NWC; w0 += 32) {
+      const int w = w0 + tid;
+      int cnt = 0;
+      if (w < NWC) {
+        const int r = w / NW, u = w % NW;
+        int gx = x0 - 2 + u, gy = y - 1 + r, gs = 0;
+        bool ok = gx >= 0 && gx < nx && gy >= 0 && gy < ny;
+        if (ok || ((gx >= 0 && gx < nx) || e.wrapx) && ((gy >= 0 && gy < ny) || e.wrapy)) {
+          gx = ((gx % nx) + nx) % nx;
+          gy = ((gy % ny) + ny) % ny;
+          const int64_t cc = plane + (int64_t)gy * nx + gx;
+          gs = e.start[cc];
+          cnt = e.start[cc + 1] - gs;
+        }
+        wgs[w] = gs;
+      }
+      const int incl = warp_inclusive_scan(cnt);
+      if (w < NWC) wst[w + 1] = tot + incl;
+      tot += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (tid == 0) wst[0] = 0;
+  }
+  __syncthreads();
+  const int W = wst[NWC];
+  const bool win_sm = W <= S::WCAP;
+
+  auto find_cell = [&](int m) {  // last w with wst[w] <= m
+    int lo = 0, hi = NWC;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (wst[mid] <= m) lo = mid; else hi = mid;
+    }
+    return lo;
+  };
+  auto member_id = [&](int m, int w) { return __ldg(e.items + wgs[w] + (m - wst[w])); };
+  if (win_sm) {
+    for (int m = tid; m < W; m += BT) {
+      const int w = find_cell(m);
+      const int j = member_id(m, w);
+      sid[m] = j;
+      skey[m] = a.ids ? __ldg(a.ids + j) : j;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) scrd[k * S::WCAP + m] = __double2half(__ldg(e.x[k] + j));
+    }
+  }
+  auto key_of = [&](int m) -> int {
+    if (win_sm) return skey[m];
+    const int j = member_id(m, find_cell(m));
+    return a.ids ? __ldg(a.ids + j) : j;
+  };
+
+  // the CTA's runs: chunk span from the scanned run starts
+  if (tid == 0) {
+    s_ch0 = e.cstart[plane + (int64_t)y * nx + x0];
+    s_nch = (int)(e.cstart[plane + (int64_t)y * nx + x1] - s_ch0);
+  }
+  for (int v = tid; v < nrun; v += BT) {
+    const int64_t c = plane + (int64_t)y * nx + x0 + v;
+    a.tri[c] = make_int2(e.cstart[c], e.cstart[c + 1]);
+  }
+  __syncthreads();
+  const int64_t ch0 = s_ch0;
+  const int nch = s_nch;
+  const bool out_sm = nch <= S::OCAP;
+  const __half nanv = hbits(0x7E00u);
+  if (out_sm) {
+    for (int q = tid; q < nch * 4; q += BT) {
+      const int c = q >> 2, l = q & 3;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) *rec_el<3, FP16, MODE_RCLL>(sch, c, k, l) = nanv;
+      *rec_el<3, FP16, MODE_RCLL>(sch, c, 3, l) = hbits(0);
+      *rec_el<3, FP16, MODE_RCLL>(sch, c, 4, l) = hbits(0);
+      stag[q] = 0xFFFFFFFFu;
+    }
+  } else {
+    for (int v = tid; v < nrun; v += BT) {  // pad records of each run
+      const int64_t c = plane + (int64_t)y * nx + x0 + v;
+      const int64_t r0 = 4 * (int64_t)e.cstart[c], r1 = 4 * (int64_t)e.cstart[c + 1];
+      int len = 0;
+      for (int rr = 0; rr < 3; ++rr)
+        for (int uu = v + 1; uu <= v + 3; ++uu) len += wst[rr * NW + uu + 1] - wst[rr * NW + uu];
+      for (int64_t q = r0 + len; q < r1; ++q) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) store_el<3, FP16, MODE_RCLL>(a.qc, q, k, nanv);
+        store_el<3, FP16, MODE_RCLL>(a.qc, q, 3, hbits(0));
+        store_el<3, FP16, MODE_RCLL>(a.qc, q, 4, hbits(0));
+        reinterpret_cast<unsigned*>(a.qtag)[q] = 0xFFFFFFFFu;
+      }
+    }
+  }
+  __syncthreads();
+
+  auto less_in = [&](int w, int key) {  // keys below `key` in window cell w (lower bound)
+    const int lo = wst[w];
+    int base = lo, len = wst[w + 1] - lo;
+    if (win_sm) {
+      while (len > 0) {
+        const int half = len >> 1;
+        const bool go = skey[base + half] < key;
+        base = go ? base + half + 1 : base;
+        len = go ? len - half - 1 : half;
+      }
+    } else {
+      while (len > 0) {
+        const int half = len >> 1;
+        const bool go = key_of(base + half) < key;
+        base = go ? base + half + 1 : base;
+        len = go ? len - half - 1 : half;
+      }
+    }
+    return base - lo;
+  };
+
+  // records: members of window columns 1 .. nrun+2 (x0-1 .. x1) in all three rows
+  for (int m = tid; m < W; m += BT) {
+    const int w = find_cell(m);
+    const int r = w / NW, u = w % NW;
+    if (u < 1 || u > nrun + 2) continue;
+    const int idx = m - wst[w];
+    const int key = key_of(m);
+    const int j = win_sm ? sid[m] : member_id(m, w);
+    __half c[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      c[k] = win_sm ? scrd[k * S::WCAP + m] : __double2half(__ldg(e.x[k] + j));
+    // keys below `key` in every window cell of columns u-2 .. u+2 (own cell: idx)
+    int lt[3][5];
+#pragma unroll
+    for (int rr = 0; rr < 3; ++rr)
+#pragma unroll
+      for (int du = 0; du < 5; ++du) {
+        const int uu = u - 2 + du;
+        lt[rr][du] = (rr == r && du == 2) ? idx : ((uu >= 0 && uu < NW) ? less_in(rr * NW + uu, key) : 0);
+      }
+#pragma unroll
+    for (int dv = -1; dv <= 1; ++dv) {  // runs centred at window column v = u + dv
+      const int v = u + dv;
+      if (v < 2 || v >= nrun + 2) continue;
+      int pos = 0;
+#pragma unroll
+      for (int rr = 0; rr < 3; ++rr)
+#pragma unroll
+        for (int du = 1 + dv; du <= 3 + dv; ++du) pos += lt[rr][du];
+      const int64_t cidx = plane + (int64_t)y * nx + (x0 + v - 2);
+      const int64_t rec = 4 * (int64_t)e.cstart[cidx] + pos;
+      const __half dcx = hbits(dv == 1 ? 0x3C00u : (dv == -1 ? 0xBC00u : 0u));  // v - u
+      const __half dcy = hbits(r == 0 ? 0x3C00u : (r == 2 ? 0xBC00u : 0u));    // 1 - r
+      const uint32_t tag = a.ids ? (uint32_t)key : (uint32_t)j;
+      if (out_sm) {
+        const int lr = (int)(rec - 4 * ch0);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) *rec_el<3, FP16, MODE_RCLL>(sch, lr >> 2, k, lr & 3) = c[k];
+        *rec_el<3, FP16, MODE_RCLL>(sch, lr >> 2, 3, lr & 3) = dcx;
+        *rec_el<3, FP16, MODE_RCLL>(sch, lr >> 2, 4, lr & 3) = dcy;
+        stag[lr] = tag;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) store_el<3, FP16, MODE_RCLL>(a.qc, rec, k, c[k]);
+        store_el<3, FP16, MODE_RCLL>(a.qc, rec, 3, dcx);
+        store_el<3, FP16, MODE_RCLL>(a.qc, rec, 4, dcy);
+        reinterpret_cast<uint32_t*>(a.qtag)[rec] = tag;
+      }
+      if (dv == 0 && r == 1) {  // own cell: pos_own and the self record
+        a.selfpos[j] = (int)rec;
+        reinterpret_cast<uint2*>(const_cast<void*>(a.pos_own))[j] =
+            make_uint2(h2u(__halves2half2(c[0], c[1])), h2u(__halves2half2(c[2], hbits(0))));
+      }
+    }
+  }
+  __syncthreads();
+  if (out_sm) {
+    const uint4* src = reinterpret_cast<const uint4*>(sch);
+    uint4* dst = reinterpret_cast<uint4*>(static_cast<char*>(a.qc) + ch0 * L::BYTES);
+    for (int q = tid; q < nch * 3; q += BT) dst[q] = src[q];
+    const uint4* ts = reinterpret_cast<const uint4*>(stag);
+    uint4* td = reinterpret_cast<uint4*>(a.qtag) + ch0;
+    for (int q = tid; q < nch; q += BT) td[q] = ts[q];
+  }
+  (void)lane;
+}
+
 template <int D, int P, int M>
 static int encode_cells(int64_t C, int nx, int wrapx, const PrecConsts& pc,
                         const double* const x[3], const int32_t* items, const int32_t* start,
@@ -1855,6 +2139,33 @@ static int encode_t(int mode, int n, int64_t C, int nx, int wrapx, const PrecCon
     return 2;
   }
   if (C == 0) return 0;
+  if constexpr (D == 3 && P == FP16) {
+    if (mode == MODE_RCLL) {  // xy-plane runs: lengths -> scan -> records
+      const int ny = a.g.counts[1];
+      k_xy_runlen<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(C, nx, ny, wrapx, a.g.wrap[1], start,
+                                                                 a.xy_nch);
+      const int64_t nt = scan_tiles(C);
+      cudaMemsetAsync(a.xy_tiles, 0, sizeof(unsigned long long) * (nt + 2), st);
+      launch_scan_counts(a.xy_nch, a.xy_cstart, C, a.xy_tiles,
+                         reinterpret_cast<int*>(a.xy_tiles + nt + 1), st);
+      EncArgs e;
+      e.nx = nx;
+      e.nxb = (nx + XYShape::XB - 1) / XYShape::XB;
+      e.wrapx = wrapx;
+      e.ny = ny;
+      e.wrapy = a.g.wrap[1];
+      e.nrows = C / nx;
+      e.start = start;
+      e.items = items;
+      for (int k = 0; k < 3; ++k) e.x[k] = x[k];
+      e.pc = pc;
+      e.cstart = a.xy_cstart;
+      constexpr size_t smem = xy_smem_bytes();
+      cudaFuncSetAttribute(k_encode_xy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k_encode_xy<<<(unsigned)(e.nrows * e.nxb), XYShape::BT, smem, st>>>(e, a);
+      return 3;
+    }
+  }
   if (mode == MODE_RCLL) return encode_cells<D, P, MODE_RCLL>(C, nx, wrapx, pc, x, items, start, a, st);
   return encode_cells<D, P, MODE_CLL>(C, nx, wrapx, pc, x, items, start, a, st);
 }
