@@ -342,7 +342,7 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
   a.qc = ctx->qc.p;
   a.nchunks = chunks;
   a.qtag = ctx->qtag.p;
-  a.selfpos = ctx->selfpos.as<int32_t>();
+  a.selfpos = ctx->selfpos.as<uint32_t>();
   a.xy_nch = ctx->xy_nch.as<int32_t>();
   a.xy_cstart = ctx->xy_cstart.as<int32_t>();
   a.xy_tiles = ctx->xy_tiles.as<unsigned long long>();

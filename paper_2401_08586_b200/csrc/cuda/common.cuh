@@ -42,7 +42,7 @@ struct SweepArgs {
                               // for CLL), then the RCLL x offset quad dc = cx_i - cx_j
   void* qtag;                 // [chunks] uint4 particle ids (~0 = sentinel)
   int64_t nchunks;            // chunks allocated for qc / qtag
-  int32_t* selfpos;           // [n] record index of particle i in its own-cell run
+  uint32_t* selfpos;          // [n] record index of particle i in its own-cell run (< 2^32)
   const void* pos_own;        // packed coords in particle order
   const int32_t* cellk[3];    // RCLL: RelCoords::cell[k] (particle order)
   const int32_t* cell_of;     // CLL:  CellGrid::cell_of  (particle order)

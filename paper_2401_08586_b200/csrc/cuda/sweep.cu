@@ -847,9 +847,9 @@ __global__ void __launch_bounds__(BT, R16Shape<D>::MINB) k_rcll16(SweepArgs a) {
       hh2[k] = __half2half2(hbits(a.c.h_hh[k]));
     }
   }
-  const int self = __ldg(a.selfpos + i);
-  const int selfch = self >> 2;
-  const unsigned selfmask = ~(1u << (28 + (self & 3)));
+  const unsigned self = __ldg(a.selfpos + i);  // record index (may exceed 2^31)
+  const int selfch = (int)(self >> 2);
+  const unsigned selfmask = ~(1u << (28 + (self & 3u)));
 
   // the particle's non-empty runs, (dz, dy) ascending
   int nruns = 0;
@@ -1033,9 +1033,9 @@ struct R16Own {
     thr2 = __half2half2(hbits(a.c.h_thr));
     hcy = a.c.h_cc[1];
     hcz = a.c.h_cc[2];
-    const int self = __ldg(a.selfpos + i);
-    selfch = self >> 2;
-    selfmask = ~(1u << (28 + (self & 3)));
+    const unsigned self = __ldg(a.selfpos + i);  // record index (may exceed 2^31)
+    selfch = (int)(self >> 2);
+    selfmask = ~(1u << (28 + (self & 3u)));
   }
   // hit word of chunks [g, e) of the run in slot q
   template <int Q>
@@ -1369,9 +1369,9 @@ __global__ void __launch_bounds__(BT) k_sweep(SweepArgs a) {
   int k = 0;
   if (valid) {
     tst.init(a, i);
-    const int self = MODE == MODE_ALL ? i : __ldg(a.selfpos + i);
-    selfch = self >> 2;
-    selfmask = ~(1u << (28 + (self & 3)));
+    const unsigned self = MODE == MODE_ALL ? (unsigned)i : __ldg(a.selfpos + i);
+    selfch = (int)(self >> 2);
+    selfmask = ~(1u << (28 + (self & 3u)));
     int w = 0;
     walk_groups<D, P, MODE>(a, i, tst, [&](const typename Tst::Row& row, bool own, int g, int e) {
       const unsigned word = group_word<D, P, MODE>(a, tst, row, own, selfch, selfmask, g, e);
@@ -1812,7 +1812,7 @@ __global__ void __launch_bounds__(EncShape<D, P>::BT) k_encode_rows(EncArgs e, S
         reinterpret_cast<uint32_t*>(a.qtag)[rec] = tag;
       }
       if (Lr == 1) {  // own cell: pos_own and the self record
-        a.selfpos[j] = (int)rec;
+        a.selfpos[j] = (uint32_t)rec;
         T own[3] = {c[0], D > 1 ? c[1] : T(0.0f), D > 2 ? c[2] : T(0.0f)};
         typename Coord<D, P>::T pk;
         if constexpr (P == FP16) {
@@ -2088,7 +2088,7 @@ __global__ void __launch_bounds__(XYShape::BT) k_encode_xy(EncArgs e, SweepArgs 
         reinterpret_cast<uint32_t*>(a.qtag)[rec] = tag;
       }
       if (dv == 0 && r == 1) {  // own cell: pos_own and the self record
-        a.selfpos[j] = (int)rec;
+        a.selfpos[j] = (uint32_t)rec;
         reinterpret_cast<uint2*>(const_cast<void*>(a.pos_own))[j] =
             make_uint2(h2u(__halves2half2(c[0], c[1])), h2u(__halves2half2(c[2], hbits(0))));
       }
