@@ -1895,7 +1895,7 @@ struct XYShape {
 };
 
 constexpr size_t xy_smem_bytes() {
-  return (size_t)XYShape::WCAP * (4 + 4 + 3 * 2) + (size_t)XYShape::OCAP * (48 + 16);
+  return (size_t)XYShape::WCAP * (4 + 4 + 4 + 2 + 1) + (size_t)XYShape::OCAP * (48 + 16);
 }
 
 __global__ void __launch_bounds__(XYShape::BT) k_encode_xy(EncArgs e, SweepArgs a) {
@@ -1903,17 +1903,20 @@ __global__ void __launch_bounds__(XYShape::BT) k_encode_xy(EncArgs e, SweepArgs 
   using L = ChunkLay<3, FP16, MODE_RCLL>;
   constexpr int XB = S::XB, BT = S::BT, NW = S::NW, NWC = 3 * NW;
   extern __shared__ __align__(16) unsigned char sm[];
-  int32_t* skey = reinterpret_cast<int32_t*>(sm);
-  int32_t* sid = skey + S::WCAP;
-  __half* scrd = reinterpret_cast<__half*>(sid + S::WCAP);  // [3][WCAP]
-  unsigned char* sch = sm + (size_t)S::WCAP * 14;            // [OCAP][48]
+  int32_t* skey = reinterpret_cast<int32_t*>(sm);              // merge key, window order
+  int32_t* sid = skey + S::WCAP;                                // particle id
+  int32_t* sstrip = sid + S::WCAP;                              // keys of each column strip, sorted
+  int16_t* srank = reinterpret_cast<int16_t*>(sstrip + S::WCAP); // rank in the member's strip
+  uint8_t* sw = reinterpret_cast<uint8_t*>(srank + S::WCAP);     // window cell of the member
+  unsigned char* sch = sm + (size_t)S::WCAP * 15;               // [OCAP][48]
   uint32_t* stag = reinterpret_cast<uint32_t*>(sch + (size_t)S::OCAP * L::BYTES);
   __shared__ int wst[NWC + 1];   // window member offset of window cell w = r * NW + u
   __shared__ int wgs[NWC];       // CSR slot of window cell w's first member
+  __shared__ int sst[NW + 1];    // strip member offset of window column u (its 3 cells)
   __shared__ int64_t s_ch0;
   __shared__ int s_nch;
 
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x;
   const int nx = e.nx, ny = e.ny;
   const int64_t row = blockIdx.x / e.nxb;        // (y, z) row of the centre cells
   const int x0 = (int)(blockIdx.x % e.nxb) * XB;
@@ -1946,6 +1949,13 @@ __global__ void __launch_bounds__(XYShape::BT) k_encode_xy(EncArgs e, SweepArgs 
       tot += __shfl_sync(0xffffffffu, incl, 31);
     }
     if (tid == 0) wst[0] = 0;
+    __syncwarp();
+    int scnt = 0;  // strips: NW <= 32 columns, one lane each
+    if (tid < NW)
+      for (int r = 0; r < 3; ++r) scnt += wst[r * NW + tid + 1] - wst[r * NW + tid];
+    const int sincl = warp_inclusive_scan(scnt);
+    if (tid < NW) sst[tid + 1] = sincl;
+    if (tid == 0) sst[0] = 0;
   }
   __syncthreads();
   const int W = wst[NWC];
@@ -1966,8 +1976,7 @@ __global__ void __launch_bounds__(XYShape::BT) k_encode_xy(EncArgs e, SweepArgs 
       const int j = member_id(m, w);
       sid[m] = j;
       skey[m] = a.ids ? __ldg(a.ids + j) : j;
-#pragma unroll
-      for (int k = 0; k < 3; ++k) scrd[k * S::WCAP + m] = __double2half(__ldg(e.x[k] + j));
+      sw[m] = (uint8_t)w;
     }
   }
   auto key_of = [&](int m) -> int {
@@ -2015,7 +2024,6 @@ __global__ void __launch_bounds__(XYShape::BT) k_encode_xy(EncArgs e, SweepArgs 
       }
     }
   }
-  __syncthreads();
 
   auto less_in = [&](int w, int key) {  // keys below `key` in window cell w (lower bound)
     const int lo = wst[w];
@@ -2038,36 +2046,18 @@ __global__ void __launch_bounds__(XYShape::BT) k_encode_xy(EncArgs e, SweepArgs 
     return base - lo;
   };
 
-  // records: members of window columns 1 .. nrun+2 (x0-1 .. x1) in all three rows
-  for (int m = tid; m < W; m += BT) {
-    const int w = find_cell(m);
-    const int r = w / NW, u = w % NW;
-    if (u < 1 || u > nrun + 2) continue;
-    const int idx = m - wst[w];
-    const int key = key_of(m);
-    const int j = win_sm ? sid[m] : member_id(m, w);
+  // place member m (window cell w, merge key `key`, id j) in the runs centred at
+  // window columns u-1 .. u+1; col[du] = keys below `key` in window column u-2+du
+  auto place = [&](int m, int w, int key, int j, const int (&col)[5]) {
+    const int r = w / NW, u = w - r * NW;
     __half c[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k)
-      c[k] = win_sm ? scrd[k * S::WCAP + m] : __double2half(__ldg(e.x[k] + j));
-    // keys below `key` in every window cell of columns u-2 .. u+2 (own cell: idx)
-    int lt[3][5];
-#pragma unroll
-    for (int rr = 0; rr < 3; ++rr)
-#pragma unroll
-      for (int du = 0; du < 5; ++du) {
-        const int uu = u - 2 + du;
-        lt[rr][du] = (rr == r && du == 2) ? idx : ((uu >= 0 && uu < NW) ? less_in(rr * NW + uu, key) : 0);
-      }
+    for (int k = 0; k < 3; ++k) c[k] = __double2half(__ldg(e.x[k] + j));
 #pragma unroll
     for (int dv = -1; dv <= 1; ++dv) {  // runs centred at window column v = u + dv
       const int v = u + dv;
       if (v < 2 || v >= nrun + 2) continue;
-      int pos = 0;
-#pragma unroll
-      for (int rr = 0; rr < 3; ++rr)
-#pragma unroll
-        for (int du = 1 + dv; du <= 3 + dv; ++du) pos += lt[rr][du];
+      const int pos = col[1 + dv] + col[2 + dv] + col[3 + dv];
       const int64_t cidx = plane + (int64_t)y * nx + (x0 + v - 2);
       const int64_t rec = 4 * (int64_t)e.cstart[cidx] + pos;
       const __half dcx = hbits(dv == 1 ? 0x3C00u : (dv == -1 ? 0xBC00u : 0u));  // v - u
@@ -2093,6 +2083,78 @@ __global__ void __launch_bounds__(XYShape::BT) k_encode_xy(EncArgs e, SweepArgs 
             make_uint2(h2u(__halves2half2(c[0], c[1])), h2u(__halves2half2(c[2], hbits(0))));
       }
     }
+    (void)m;
+  };
+
+  if (win_sm) {
+    // strips: the three cells of each window column id-merged (rank = index in own
+    // cell + keys below in the column's two other cells)
+    for (int m = tid; m < W; m += BT) {
+      const int w = sw[m];
+      const int r = w / NW, u = w - r * NW;
+      const int key = skey[m];
+      int sr = m - wst[w];
+#pragma unroll
+      for (int rr = 0; rr < 3; ++rr)
+        if (rr != r) sr += less_in(rr * NW + u, key);
+      sstrip[sst[u] + sr] = key;
+      srank[m] = (int16_t)sr;
+    }
+    __syncthreads();
+    auto strip_less = [&](int u, int key) {  // keys below `key` in strip u
+      const int lo = sst[u], len = sst[u + 1] - lo;
+      int base = 0;
+      if (len < 64) {
+#pragma unroll
+        for (int st = 32; st > 0; st >>= 1) {
+          const int t = base + st;
+          if (t <= len && sstrip[lo + t - 1] < key) base = t;
+        }
+      } else {
+        int n = len;
+        while (n > 0) {
+          const int half = n >> 1;
+          const bool go = sstrip[lo + base + half] < key;
+          base = go ? base + half + 1 : base;
+          n = go ? n - half - 1 : half;
+        }
+      }
+      return base;
+    };
+    // records: members of window columns 1 .. nrun+2 (x0-1 .. x1)
+    for (int m = tid; m < W; m += BT) {
+      const int w = sw[m];
+      const int u = w % NW;
+      if (u < 1 || u > nrun + 2) continue;
+      const int key = skey[m];
+      int col[5];
+#pragma unroll
+      for (int du = 0; du < 5; ++du) {
+        const int uu = u - 2 + du;
+        col[du] = du == 2 ? (int)srank[m] : ((uu >= 0 && uu < NW) ? strip_less(uu, key) : 0);
+      }
+      place(m, w, key, sid[m], col);
+    }
+  } else {
+    __syncthreads();
+    for (int m = tid; m < W; m += BT) {
+      const int w = find_cell(m);
+      const int r = w / NW, u = w % NW;
+      if (u < 1 || u > nrun + 2) continue;
+      const int idx = m - wst[w];
+      const int key = key_of(m);
+      int col[5];
+#pragma unroll
+      for (int du = 0; du < 5; ++du) {
+        const int uu = u - 2 + du;
+        int s = 0;
+#pragma unroll
+        for (int rr = 0; rr < 3; ++rr)
+          s += (rr == r && du == 2) ? idx : ((uu >= 0 && uu < NW) ? less_in(rr * NW + uu, key) : 0);
+        col[du] = s;
+      }
+      place(m, w, key, member_id(m, w), col);
+    }
   }
   __syncthreads();
   if (out_sm) {
@@ -2103,7 +2165,6 @@ __global__ void __launch_bounds__(XYShape::BT) k_encode_xy(EncArgs e, SweepArgs 
     uint4* td = reinterpret_cast<uint4*>(a.qtag) + ch0;
     for (int q = tid; q < nch; q += BT) td[q] = ts[q];
   }
-  (void)lane;
 }
 
 template <int D, int P, int M>
