@@ -1131,13 +1131,22 @@ __global__ void __launch_bounds__(BT, R16Two<D>::EMINB) k_r16_emit(SweepArgs a) 
     r16_runs<D>(a, i, true, cb, ce);
     R16Own<D> own;
     if (ovf) own.init(a, i);
-    int kk = 0, w = 0;
+    int kk = 0, w = 0, ng = 0;
+#pragma unroll
+    for (int q = 0; q < NR; ++q) ng += (ce[q] - cb[q] + 7) >> 3;
+    ng = min(ng, W);
+    // hit words four groups ahead of their use (independent loads in flight)
+    auto ldw = [&](int v) { return v < ng ? __ldg(a.hitw + (int64_t)v * a.nrows + r) : 0u; };
+    unsigned h0 = ldw(0), h1 = ldw(1), h2 = ldw(2), h3 = ldw(3);
     r16_for_slots<D, 0>([&](auto qv) {
       constexpr int Q = decltype(qv)::value;
       const int gs = kk;
       for (int g = cb[Q]; g < ce[Q]; g += 8) {
-        unsigned word = w < W ? __ldg(a.hitw + (int64_t)w * a.nrows + r)
-                              : own.template group<Q>(qc, g, min(g + 8, ce[Q]));
+        unsigned word = w < W ? h0 : own.template group<Q>(qc, g, min(g + 8, ce[Q]));
+        h0 = h1;
+        h1 = h2;
+        h2 = h3;
+        h3 = ldw(w + 4);
         ++w;
         while (word) {  // next chunk with hits
           const int sh = (__ffs(word) - 1) & ~3;
