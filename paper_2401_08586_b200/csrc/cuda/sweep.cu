@@ -1135,9 +1135,9 @@ __global__ void __launch_bounds__(BT, R16Two<D>::EMINB) k_r16_emit(SweepArgs a) 
 #pragma unroll
     for (int q = 0; q < NR; ++q) ng += (ce[q] - cb[q] + 7) >> 3;
     ng = min(ng, W);
-    // hit words four groups ahead of their use (independent loads in flight)
+    // hit words six groups ahead of their use (independent loads in flight)
     auto ldw = [&](int v) { return v < ng ? __ldg(a.hitw + (int64_t)v * a.nrows + r) : 0u; };
-    unsigned h0 = ldw(0), h1 = ldw(1), h2 = ldw(2), h3 = ldw(3);
+    unsigned h0 = ldw(0), h1 = ldw(1), h2 = ldw(2), h3 = ldw(3), h4 = ldw(4), h5 = ldw(5);
     r16_for_slots<D, 0>([&](auto qv) {
       constexpr int Q = decltype(qv)::value;
       const int gs = kk;
@@ -1146,7 +1146,9 @@ __global__ void __launch_bounds__(BT, R16Two<D>::EMINB) k_r16_emit(SweepArgs a) 
         h0 = h1;
         h1 = h2;
         h2 = h3;
-        h3 = ldw(w + 4);
+        h3 = h4;
+        h4 = h5;
+        h5 = ldw(w + 6);
         ++w;
         while (word) {  // next chunk with hits
           const int sh = (__ffs(word) - 1) & ~3;
