@@ -752,9 +752,16 @@ __device__ __forceinline__ void r16_chunk(const char* __restrict__ qc, int ch, c
       a[h] = acc2;
     }
   } else {
-    const uint4* p = reinterpret_cast<const uint4*>(qc + (size_t)ch * 32);
-    const uint4 v0 = __ldg(p);
-    const uint2 v1 = __ldg(reinterpret_cast<const uint2*>(p + 1));
+    // the 32-byte record is one sector: one 256-bit load (LDG.256, sm_100)
+    uint4 v0;
+    uint2 v1;
+    unsigned pad0, pad1;
+    asm("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(v0.x), "=r"(v0.y), "=r"(v0.z), "=r"(v0.w), "=r"(v1.x), "=r"(v1.y), "=r"(pad0),
+          "=r"(pad1)
+        : "l"(qc + (size_t)ch * 32));
+    (void)pad0;
+    (void)pad1;
     // quads: x = (v0.x, v0.y), y = (v0.z, v0.w), dc = (v1.x, v1.y)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
