@@ -28,6 +28,8 @@
  *   sphx_rcll_grad_normalized(_device)
  *                        <- grad_normalized(f, ps, rcll(rc, grid, fp16), kp) fused
  *                                                                   gradient.cpp:44-82, dynamics.cpp:145-155
+ *   sphx_step_mixed_device <- StepResult step_mixed(MixedState&, const StepConfig&)
+ *                                                                   dynamics.cpp:136-203
  *   sphx_table_distances / sphx_rcll_distances_device
  *                        <- double rel_distance(const RelCoords&, size_t i, size_t j,
  *                                               const CellGrid&, Precision) for every entry
@@ -257,6 +259,51 @@ int sphx_rcll_grad_normalized_device(sphx_context* ctx, const sphx_grid_desc* gr
                                      int32_t precision, const double* const d_x[3],
                                      const double* d_f, double h, double* const d_g[3],
                                      unsigned long long* d_degenerate);
+
+/* ---------------- the mixed-precision time step ----------------
+ * step_mixed(MixedState&, const StepConfig&) (dynamics.hpp:84-107, dynamics.cpp:136-203)
+ * on device memory: the approach's neighbour search (I: cell_link_list FP64, II:
+ * cell_link_list FP16, III: rcll FP16), apply_eos, assemble_newtonian_stress, the
+ * FP64 rates (rhs_density / rhs_momentum / rhs_energy), the symplectic Euler
+ * kick-drift with periodic wrap, then update_relative (FP64) + rebuild_members
+ * (III) or rebin (I, II). Every field is bit-identical to the reference. The
+ * step's table goes to d_offsets / d_items_out; when it needs more than
+ * `capacity` entries the call returns SPHX_ERR_CAPACITY with *total set and the
+ * state untouched. StepConfig::pre_force (a C++ callback) has no counterpart:
+ * run it between steps. On an update_relative / rebin error every particle has
+ * already moved (the reference stops at the first offending particle). */
+#define SPHX_APPROACH_I 0
+#define SPHX_APPROACH_II 1
+#define SPHX_APPROACH_III 2
+
+typedef struct sphx_step_config { /* StepConfig (dynamics.hpp:84-96) */
+  double dt, c_sound, rho0, mu;
+  double body_force[3];
+  int64_t n_moving;       /* 0: every particle moves */
+  int32_t evolve_density; /* the reference's default is 1 */
+  int32_t compute_energy;
+} sphx_step_config;
+
+typedef struct sphx_mixed_state_device { /* MixedState (dynamics.hpp:71-82), device memory */
+  int64_t n;
+  double h;                            /* ParticleSystem::h() */
+  double* x[3];
+  double* v[3];
+  const double* m;
+  double* rho;
+  double* p;
+  double* e;
+  double* rel[3];                      /* RelCoords (approach III) */
+  int32_t* cell[3];
+  int32_t* cell_of;                    /* CellGrid membership (CSR) */
+  int32_t* cell_start;
+  int32_t* items;
+} sphx_mixed_state_device;
+
+int sphx_step_mixed_device(sphx_context* ctx, const sphx_grid_desc* grid, int32_t approach,
+                           const sphx_mixed_state_device* state, const sphx_step_config* cfg,
+                           int64_t* d_offsets, int32_t* d_items_out, int64_t capacity,
+                           double* max_dx, int64_t* total);
 
 /* Un-jittered build_lattice sites with ids [id0, id0 + count) written to d_x
  * (x_k = lo_k + (c_k + 0.5) ds, bit-identical to particle_system.cpp:53). */

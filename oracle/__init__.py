@@ -130,6 +130,14 @@ def _bind_ref(lib):
             "ref_grad_normalized": (C.c_int64, [vp, vp, vp, C.c_double, vp, vp, vp]),
             "ref_update_relative": (C.c_int64, [vp, vp, C.c_uint64, vp, vp, vp, C.c_int]),
             "ref_time_nnps": (C.c_double, [C.c_int, vp, vp, vp, C.c_int, C.c_int]),
+            "ref_mixed_new": (vp, [vp, C.POINTER(C.c_int), C.c_int]),
+            "ref_mixed_free": (None, [vp]),
+            "ref_mixed_get": (None, [vp, C.c_int, C.c_int, vp]),
+            "ref_mixed_set": (None, [vp, C.c_int, C.c_int, vp]),
+            "ref_mixed_grid": (None, [vp, vp, vp, vp]),
+            "ref_mixed_step": (C.c_int, [vp, d3, d3, C.c_uint64, C.c_int, C.c_int,
+                                         C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+            "ref_mixed_table": (None, [vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)
@@ -335,6 +343,69 @@ class RefSystem:
     def time_nnps(self, backend: str, prec: int, repeats: int = 5) -> float:
         which = 0 if backend == "rcll" else 1
         return float(self.lib.ref_time_nnps(which, self.ps, self.rel, self.grid, prec, repeats))
+
+
+class RefMixed:
+    """The reference's MixedState (dynamics.hpp:71-82) and step_mixed
+    (dynamics.cpp:136-203), through the compiled reference library."""
+
+    FIELDS = {"x": 0, "v": 1, "rho": 2, "p": 3, "e": 4, "m": 5, "rel": 6}
+
+    def __init__(self, system: "RefSystem", periodic, approach: int):
+        self.lib = system.lib
+        per = (C.c_int * 3)(*[int(bool(p)) for p in list(periodic) + [0] * 3][:3])
+        self.st = self.lib.ref_mixed_new(system.ps, per, approach)
+        if not self.st:
+            raise RefError(self.lib.ref_last_error().decode())
+        self.n, self.dim = system.n, system.dim
+
+    def __del__(self):
+        try:
+            if self.st:
+                self.lib.ref_mixed_free(self.st)
+        except Exception:
+            pass
+
+    def get(self, name: str, k: int = 0) -> np.ndarray:
+        if name == "cell":
+            out = np.empty(self.n, np.int32)
+            self.lib.ref_mixed_get(self.st, 7, k, out.ctypes.data)
+            return out
+        out = np.empty(self.n, np.float64)
+        self.lib.ref_mixed_get(self.st, self.FIELDS[name], k, out.ctypes.data)
+        return out
+
+    def set(self, name: str, k: int, values) -> None:
+        a = np.ascontiguousarray(values, np.float64)
+        assert a.size == self.n
+        self.lib.ref_mixed_set(self.st, self.FIELDS[name], k, a.ctypes.data)
+
+    def grid_members(self, cells: int):
+        cell_of = np.empty(self.n, np.int32)
+        start = np.empty(cells + 1, np.int32)
+        items = np.empty(self.n, np.int32)
+        self.lib.ref_mixed_grid(self.st, cell_of.ctypes.data, start.ctypes.data, items.ctypes.data)
+        return cell_of, start, items
+
+    def step(self, dt, c_sound, rho0=1.0, mu=0.0, body_force=(0, 0, 0), n_moving=0,
+             evolve_density=True, compute_energy=False):
+        """One step_mixed; returns (max_dx, table total). Raises RefError with the
+        reference's message when it throws."""
+        mx = C.c_double()
+        tot = C.c_int64()
+        rc = self.lib.ref_mixed_step(self.st, (C.c_double * 4)(dt, c_sound, rho0, mu),
+                                     _d3(list(body_force) + [0] * (3 - len(body_force))),
+                                     n_moving, int(evolve_density), int(compute_energy),
+                                     C.byref(mx), C.byref(tot))
+        if rc != 0:
+            raise RefError(self.lib.ref_last_error().decode())
+        return mx.value, tot.value
+
+    def table(self, total: int):
+        off = np.empty(self.n + 1, np.int64)
+        it = np.empty(total, np.int32)
+        self.lib.ref_mixed_table(self.st, off.ctypes.data, it.ctypes.data)
+        return off, it
 
 
 # --------------------------------------------------------------------------------------

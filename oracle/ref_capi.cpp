@@ -25,6 +25,7 @@
 #include "sphx/binary16.hpp"
 #include "sphx/cell_grid.hpp"
 #include "sphx/detail/nnps_batch.hpp"
+#include "sphx/dynamics.hpp"
 #include "sphx/gradient.hpp"
 #include "sphx/nnps.hpp"
 #include "sphx/particle_system.hpp"
@@ -315,6 +316,91 @@ std::int64_t ref_grad_normalized(void* ps, void* t, const double* f, double h, d
     deg = gf.degenerate_count;
   });
   return deg;
+}
+
+
+// ---- the mixed-precision time step (dynamics.cpp:136-203), SURVEY 8(f) row 3 ---------
+// A MixedState (dynamics.hpp:71-82) built from a particle system, plus the table
+// of its last step_mixed call.
+struct RefMixed {
+  sphx::MixedState st;
+  sphx::NeighborTable last;
+  RefMixed(sphx::ParticleSystem ps, std::array<bool, 3> per, sphx::Approach a)
+      : st(std::move(ps), per, a) {}
+};
+
+void* ref_mixed_new(void* ps, const int* periodic, int approach) {
+  void* out = nullptr;
+  const int rc = guarded([&] {
+    out = new RefMixed(*static_cast<sphx::ParticleSystem*>(ps),
+                       {periodic[0] != 0, periodic[1] != 0, periodic[2] != 0},
+                       static_cast<sphx::Approach>(approach));
+  });
+  return rc == 0 ? out : nullptr;
+}
+void ref_mixed_free(void* m) { delete static_cast<RefMixed*>(m); }
+
+// field: 0 x, 1 v, 2 rho, 3 p, 4 e, 5 m, 6 rel (FP64 coordinate), 7 cell (int32 out)
+static double* mixed_field(RefMixed& m, int field, int k) {
+  auto& ps = m.st.ps;
+  switch (field) {
+    case 0: return ps.x(k).data();
+    case 1: return ps.v(k).data();
+    case 2: return ps.rho().data();
+    case 3: return ps.p().data();
+    case 4: return ps.e().data();
+    case 5: return const_cast<double*>(ps.m().data());
+    case 6: return m.st.rel.rel[k].data();
+    default: return nullptr;
+  }
+}
+void ref_mixed_get(void* mp, int field, int k, double* out) {
+  auto& m = *static_cast<RefMixed*>(mp);
+  const std::size_t n = m.st.ps.size();
+  if (field == 7) {
+    std::memcpy(out, m.st.rel.cell[k].data(), sizeof(std::int32_t) * n);
+    return;
+  }
+  std::memcpy(out, mixed_field(m, field, k), sizeof(double) * n);
+}
+void ref_mixed_set(void* mp, int field, int k, const double* in) {
+  auto& m = *static_cast<RefMixed*>(mp);
+  std::memcpy(mixed_field(m, field, k), in, sizeof(double) * m.st.ps.size());
+}
+// the grid membership: cell_of (n), cell_start (cells + 1), items (n)
+void ref_mixed_grid(void* mp, std::int32_t* cell_of, std::int32_t* start, std::int32_t* items) {
+  auto& g = static_cast<RefMixed*>(mp)->st.grid;
+  const std::size_t n = static_cast<RefMixed*>(mp)->st.ps.size();
+  for (std::size_t i = 0; i < n; ++i) cell_of[i] = g.cell_of(i);
+  std::copy(g.cell_start().begin(), g.cell_start().end(), start);
+  std::copy(g.items().begin(), g.items().end(), items);
+}
+// One step_mixed with StepConfig {dt, c_sound, rho0, mu, body_force, n_moving,
+// evolve_density, compute_energy} (no pre_force). Returns 0 or the error code;
+// *max_dx and *total receive StepResult::max_dx and the table size.
+int ref_mixed_step(void* mp, const double* cfg, const double* body_force, std::uint64_t n_moving,
+                   int evolve_density, int compute_energy, double* max_dx, std::int64_t* total) {
+  auto& m = *static_cast<RefMixed*>(mp);
+  return guarded([&] {
+    sphx::StepConfig c;
+    c.dt = cfg[0];
+    c.c_sound = cfg[1];
+    c.rho0 = cfg[2];
+    c.mu = cfg[3];
+    c.body_force = {body_force[0], body_force[1], body_force[2]};
+    c.n_moving = n_moving;
+    c.evolve_density = evolve_density != 0;
+    c.compute_energy = compute_energy != 0;
+    auto res = sphx::step_mixed(m.st, c);
+    *max_dx = res.max_dx;
+    *total = res.table.total();
+    m.last = std::move(res.table);
+  });
+}
+void ref_mixed_table(void* mp, std::int64_t* offsets, std::int32_t* items) {
+  const auto& t = static_cast<RefMixed*>(mp)->last;
+  std::copy(t.offsets.begin(), t.offsets.end(), offsets);
+  std::copy(t.items.begin(), t.items.end(), items);
 }
 
 // ---- timing (experiments.cpp:268-278 method: one discarded warm-up, median) -------------

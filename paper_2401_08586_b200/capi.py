@@ -101,6 +101,9 @@ def lib():
                                                 p3, C.POINTER(i64)]),
         "sphx_rcll_grad_normalized_device": (C.c_int, [vp, G, i64, p3, p3, vp, vp, i32, p3, vp,
                                                        dbl, p3, vp]),
+        "sphx_step_mixed_device": (C.c_int, [vp, G, i32, C.POINTER(MixedStateDevice),
+                                             C.POINTER(StepConfig), vp, vp, i64,
+                                             C.POINTER(dbl), C.POINTER(i64)]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -119,7 +122,26 @@ EXPORTED = ("sphx_last_error", "sphx_grid_init", "sphx_create", "sphx_destroy",
             "sphx_table_hash", "sphx_build_rel_coords_window_device", "sphx_rcll_rows_device",
             "sphx_lattice_device", "sphx_rcll_distances_device", "sphx_table_distances",
             "sphx_rcll_grad_normalized", "sphx_rcll_grad_normalized_device",
-            "sphx_update_relative", "sphx_update_relative_device", "sphx_rebuild_members_device")
+            "sphx_update_relative", "sphx_update_relative_device", "sphx_rebuild_members_device",
+            "sphx_step_mixed_device")
+
+APPROACH_I, APPROACH_II, APPROACH_III = 0, 1, 2
+
+
+class StepConfig(C.Structure):
+    """sphx_step_config = StepConfig (dynamics.hpp:84-96) without pre_force."""
+    _fields_ = [("dt", C.c_double), ("c_sound", C.c_double), ("rho0", C.c_double),
+                ("mu", C.c_double), ("body_force", C.c_double * 3), ("n_moving", C.c_int64),
+                ("evolve_density", C.c_int32), ("compute_energy", C.c_int32)]
+
+
+class MixedStateDevice(C.Structure):
+    """sphx_mixed_state_device = MixedState (dynamics.hpp:71-82) in device memory."""
+    _fields_ = [("n", C.c_int64), ("h", C.c_double), ("x", C.c_void_p * 3),
+                ("v", C.c_void_p * 3), ("m", C.c_void_p), ("rho", C.c_void_p),
+                ("p", C.c_void_p), ("e", C.c_void_p), ("rel", C.c_void_p * 3),
+                ("cell", C.c_void_p * 3), ("cell_of", C.c_void_p), ("cell_start", C.c_void_p),
+                ("items", C.c_void_p)]
 
 
 def table_hash(offsets: np.ndarray, items: np.ndarray) -> int:
@@ -282,6 +304,38 @@ class Context:
         check(lib().sphx_rebuild_members_device(self.h, C.byref(grid), cell[0].numel(),
                                                 _dptr3(cell), cell_of.data_ptr(),
                                                 cell_start.data_ptr(), items.data_ptr()))
+
+    def step_mixed_device(self, grid: GridDesc, approach: int, state: dict, cfg: dict,
+                          offsets, items_out):
+        """step_mixed (dynamics.cpp:136-203) on device tensors. `state` holds torch
+        tensors x, v (lists per axis), m, rho, p, e, rel, cell (lists), cell_of,
+        cell_start, items, and the float h; they are updated in place. Returns
+        (max_dx, table total); the step's table is in offsets / items_out."""
+        self._bind(state["rho"])
+        st = MixedStateDevice()
+        st.n = state["rho"].numel()
+        st.h = float(state["h"])
+        for k in range(3):
+            for name in ("x", "v", "rel", "cell"):
+                arr = state.get(name)
+                getattr(st, name)[k] = arr[k].data_ptr() if arr is not None and k < len(arr) else None
+        for name in ("m", "rho", "p", "e", "cell_of", "cell_start", "items"):
+            setattr(st, name, state[name].data_ptr())
+        c = StepConfig()
+        c.dt, c.c_sound = float(cfg["dt"]), float(cfg["c_sound"])
+        c.rho0, c.mu = float(cfg.get("rho0", 1.0)), float(cfg.get("mu", 0.0))
+        bf = list(cfg.get("body_force", (0.0, 0.0, 0.0))) + [0.0] * 3
+        for k in range(3):
+            c.body_force[k] = float(bf[k])
+        c.n_moving = int(cfg.get("n_moving", 0))
+        c.evolve_density = int(bool(cfg.get("evolve_density", True)))
+        c.compute_energy = int(bool(cfg.get("compute_energy", False)))
+        mx = C.c_double()
+        tot = C.c_int64()
+        check(lib().sphx_step_mixed_device(self.h, C.byref(grid), approach, C.byref(st), C.byref(c),
+                                           offsets.data_ptr(), items_out.data_ptr(),
+                                           items_out.numel(), C.byref(mx), C.byref(tot)))
+        return mx.value, tot.value
 
     def rcll_grad_normalized(self, grid: GridDesc, rel, cell, items, cell_start, prec: int, x, f,
                              h: float):

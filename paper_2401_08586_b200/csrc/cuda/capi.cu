@@ -44,6 +44,8 @@ int launch_rcll_distances(int dim, int prec, int64_t nrows, const GridConsts& g,
                           const int32_t* items, double* dist, cudaStream_t st);
 void launch_lattice(int dim, const double lo[3], double ds, const int64_t counts[3], int64_t id0,
                     int64_t count, double* const x[3], cudaStream_t st);
+int launch_step_rates(int dim, const StepArgs& a, cudaStream_t st);
+int launch_kick_drift(int dim, const StepArgs& a, cudaStream_t st);
 }  // namespace sphx_dev
 
 using namespace sphx_dev;
@@ -139,6 +141,8 @@ struct sphx_context {
   bool t_rcll = false;  // the last host table came from sphx_rcll (inputs still staged)
   // binning scratch
   Buf b_counts, b_slot, b_bad, b_tiles, b_out_cellof, b_out_start, b_out_items, b_rel[3], b_cell[3];
+  // device time step: stress (sigma, tau, eps), rates, displacement, max |dx|, status
+  Buf s_stress, s_rates, s_dx, s_flags;
 };
 
 namespace {
@@ -898,6 +902,128 @@ int sphx_rebuild_members_device(sphx_context* ctx, const sphx_grid_desc* grid, i
   TRY(ctx->b_bad.ensure(sizeof(unsigned long long)));
   return run_binning(ctx, 2, *grid, n, nullptr, d_cell, nullptr, nullptr, d_cell_of, d_cell_start,
                      d_items, ctx->b_bad.as<unsigned long long>());
+}
+
+
+// ---------------- the mixed time step on device ----------------
+
+int sphx_step_mixed_device(sphx_context* ctx, const sphx_grid_desc* grid, int32_t approach,
+                           const sphx_mixed_state_device* state, const sphx_step_config* cfg,
+                           int64_t* d_offsets, int32_t* d_items_out, int64_t capacity,
+                           double* max_dx, int64_t* total) {
+  TRY(check_ctx(ctx));
+  if (!grid || !state || !cfg || !max_dx || !total)
+    return fail(SPHX_ERR_INVALID_ARGUMENT, "null argument");
+  TRY(check_prec_dim(SPHX_FP64, grid->dim));
+  if (approach < SPHX_APPROACH_I || approach > SPHX_APPROACH_III)
+    return fail(SPHX_ERR_INVALID_ARGUMENT, "unknown approach");
+  // make_kernel (kernel.hpp:17-29): the step builds its KernelParams from ps.h()
+  if (!(state->h > 0.0)) return fail(SPHX_ERR_INVALID_ARGUMENT, "smoothing length must be positive");
+  const int64_t n = state->n;
+  const int dim = grid->dim;
+  if (cfg->n_moving < 0 || cfg->n_moving > n)
+    return fail(SPHX_ERR_INVALID_ARGUMENT, "n_moving exceeds the particle count");
+  const int64_t n_mov = cfg->n_moving == 0 ? n : cfg->n_moving;
+  *max_dx = 0.0;
+  *total = 0;
+  // (1) neighbour search per approach (dynamics.cpp:145-155)
+  if (approach == SPHX_APPROACH_III)
+    TRY(sphx_rcll_device(ctx, grid, n, state->rel, state->cell, state->items, state->cell_start,
+                         SPHX_FP16, d_offsets, d_items_out, capacity));
+  else
+    TRY(sphx_cell_link_list_device(ctx, grid, n, state->x, state->h, state->items,
+                                   state->cell_start, state->cell_of,
+                                   approach == SPHX_APPROACH_I ? SPHX_FP64 : SPHX_FP16, d_offsets,
+                                   d_items_out, capacity));
+  int64_t tot = 0;
+  if (n > 0) {
+    CK(cudaMemcpyAsync(&tot, d_offsets + n, sizeof(tot), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  *total = tot;
+  if (tot > capacity)  // nothing of the state has changed yet
+    return fail(SPHX_ERR_CAPACITY, "neighbour table needs " + std::to_string(tot) +
+                                       " entries, capacity " + std::to_string(capacity));
+  if (n == 0) return SPHX_OK;
+
+  // (2) EOS and FP64 rates (dynamics.cpp:157-164)
+  StepArgs a;
+  a.n = n;
+  a.n_mov = n_mov;
+  a.off = d_offsets;
+  a.nb = d_items_out;
+  TRY(ctx->s_stress.ensure(sizeof(double) * 18 * n));
+  TRY(ctx->s_rates.ensure(sizeof(double) * 5 * n));
+  TRY(ctx->s_dx.ensure(sizeof(double) * 3 * n));
+  TRY(ctx->s_flags.ensure(2 * sizeof(unsigned long long)));
+  double* sb = ctx->s_stress.as<double>();
+  double* rb = ctx->s_rates.as<double>();
+  for (int s = 0; s < 6; ++s) {
+    a.sig[s] = sb + (size_t)s * n;
+    a.tau[s] = sb + (size_t)(6 + s) * n;
+    a.eps[s] = sb + (size_t)(12 + s) * n;
+  }
+  a.drho = rb;
+  a.de = rb + n;
+  for (int k = 0; k < 3; ++k) {
+    a.x[k] = k < dim ? state->x[k] : nullptr;
+    a.v[k] = k < dim ? state->v[k] : nullptr;
+    a.dv[k] = rb + (size_t)(2 + k) * n;
+    a.dx[k] = ctx->s_dx.as<double>() + (size_t)k * n;
+    a.bf[k] = cfg->body_force[k];
+    a.lo[k] = grid->lo[k];
+    a.hi[k] = grid->hi[k];
+    a.span[k] = grid->hi[k] - grid->lo[k];  // Domain::span (domain.hpp:32)
+    a.per[k] = k < dim && grid->periodic[k];
+  }
+  a.m = state->m;
+  a.rho = state->rho;
+  a.p = state->p;
+  a.e = state->e;
+  a.h = state->h;
+  const double pi = 3.141592653589793;
+  const double h = state->h;
+  a.alpha = dim == 1 ? 1.0 / h : (dim == 2 ? 15.0 / (7.0 * pi * h * h) : 3.0 / (2.0 * pi * h * h * h));
+  a.mu = cfg->mu;
+  a.c2 = cfg->c_sound * cfg->c_sound;
+  a.rho0 = cfg->rho0;
+  a.dt = cfg->dt;
+  a.evolve_density = cfg->evolve_density != 0;
+  a.compute_energy = cfg->compute_energy != 0;
+  unsigned long long* flags = ctx->s_flags.as<unsigned long long>();
+  a.maxdx = flags;
+  CK(cudaMemsetAsync(flags, 0, sizeof(unsigned long long), ctx->stream));
+  ctx->launches += launch_step_rates(dim, a, ctx->stream);
+  CKL();
+  // (3)-(4) kick, drift (dynamics.cpp:166-187)
+  ctx->launches += launch_kick_drift(dim, a, ctx->stream);
+  CKL();
+  // (5) coordinate maintenance (dynamics.cpp:188-201)
+  unsigned long long st = ~0ull;
+  if (approach == SPHX_APPROACH_III) {
+    double* dxp[3] = {a.dx[0], a.dx[1], a.dx[2]};
+    TRY(sphx_update_relative_device(ctx, grid, n_mov, state->rel, state->cell, dxp, SPHX_FP64,
+                                    flags + 1));
+    TRY(sphx_rebuild_members_device(ctx, grid, n, state->cell, state->cell_of, state->cell_start,
+                                    state->items));
+  } else {
+    TRY(sphx_rebin_device(ctx, grid, n, state->x, state->cell_of, state->cell_start, state->items,
+                          reinterpret_cast<int64_t*>(flags + 1)));
+  }
+  unsigned long long hf[2] = {0, ~0ull};
+  CK(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(max_dx, &hf[0], sizeof(double));
+  st = hf[1];
+  if (st != ~0ull) {
+    if (approach == SPHX_APPROACH_III) {  // update_relative's runtime_error (cell_grid.cpp:185-205)
+      const int axis = (int)((st >> 1) & 3);
+      return fail(SPHX_ERR_RUNTIME, (st & 1) ? "particle leaves the grid on axis " + std::to_string(axis)
+                                             : "displacement skips a cell on axis " + std::to_string(axis));
+    }
+    return fail(SPHX_ERR_OUT_OF_RANGE, "particle " + std::to_string(st) + " lies outside the grid");
+  }
+  return SPHX_OK;
 }
 
 // ---------------- multi-GPU slab path ----------------

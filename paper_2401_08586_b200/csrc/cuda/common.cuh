@@ -163,4 +163,30 @@ struct LocateArgs {
   unsigned long long* bad;  // BIN_REBIN: min out-of-grid index
 };
 
+// device time step (step.cu): the state, the step's table and its scratch
+struct StepArgs {
+  int64_t n = 0, n_mov = 0;
+  const int64_t* off = nullptr;  // the step's neighbour table
+  const int32_t* nb = nullptr;
+  double* x[3] = {nullptr, nullptr, nullptr};
+  double* v[3] = {nullptr, nullptr, nullptr};
+  const double* m = nullptr;
+  double* rho = nullptr;
+  double* p = nullptr;
+  double* e = nullptr;
+  double* sig[6] = {};  // StressState (dynamics.hpp:33-37), sym_index order
+  double* tau[6] = {};
+  double* eps[6] = {};
+  double* drho = nullptr;  // rates
+  double* dv[3] = {nullptr, nullptr, nullptr};
+  double* de = nullptr;
+  double* dx[3] = {nullptr, nullptr, nullptr};  // Eq. 9 displacement of the step
+  double h = 0, alpha = 0, mu = 0, c2 = 0, rho0 = 0, dt = 0;
+  double bf[3] = {0, 0, 0};
+  int evolve_density = 1, compute_energy = 0;
+  double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0}, span[3] = {0, 0, 0};
+  int per[3] = {0, 0, 0};
+  unsigned long long* maxdx = nullptr;  // bits of the non-negative max |dx|
+};
+
 }  // namespace sphx_dev
