@@ -58,9 +58,10 @@ def parse():
     ap.add_argument("--precision", default="fp16", choices=sorted(PREC))
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--op", default="table", choices=["table", "grad"],
+    ap.add_argument("--op", default="table", choices=["table", "grad", "step"],
                     help="table: the NNPS table (default); grad: fused FP16 RCLL -> "
-                         "grad_normalized (SURVEY 8(f) row 1), no table in HBM")
+                         "grad_normalized (SURVEY 8(f) row 1), no table in HBM; step: the "
+                         "mixed time step step_mixed, approach III (SURVEY 8(f) row 3)")
     ap.add_argument("--slab", action="store_true",
                     help="use the slab-decomposed (multi-GPU) path even at N=1")
     return ap.parse_args()
@@ -345,6 +346,9 @@ def run_ours(args):
     ctx.build_rel_coords_device(grid, xd, rel, cell, cell_of, start, items)
     if args.op == "grad":
         return bench_grad(args, w, ctx, stream, grid, n, C, xd, rel, cell, items, start, local)
+    if args.op == "step":
+        return bench_step(args, w, ctx, stream, grid, n, C, xd, rel, cell, cell_of, items, start,
+                          local)
     del xd
     offsets = torch.empty(n + 1, dtype=torch.int64, device=dev)
     cap = n * (24 if dim == 2 else 60)
@@ -549,6 +553,120 @@ def bench_grad(args, w, ctx, stream, grid, n, C, xd, rel, cell, items, start, lo
         "gpu_launches": ctx.launches - launches0,
         "clocks": clk.summary(),
     }
+    print(json.dumps(line), flush=True)
+
+
+def bench_step(args, w, ctx, stream, grid, n, C, xd, rel, cell, cell_of, items, start, local):
+    """The mixed time step (step_mixed, approach III: FP16 RCLL table, EOS, stress,
+    FP64 rates, kick-drift, update_relative + rebuild_members) on device-resident
+    state; one step = one sphx_step_mixed_device call. Parity: one step from the
+    same initial state against the reference's own step_mixed (oracle/_ref), every
+    field and the table bit for bit; the reference step's time is the CPU baseline."""
+    import torch
+
+    import oracle as O
+    dev = xd[0].device
+    dim, ds = w["dim"], w["ds"]
+    h = 1.2 * ds
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(5)
+    st = {"h": h, "x": xd, "rel": rel, "cell": cell, "cell_of": cell_of, "cell_start": start,
+          "items": items,
+          "v": [0.1 * torch.randn(n, dtype=torch.float64, device=dev, generator=gen)
+                for _ in range(dim)],
+          "rho": 1.0 + 0.01 * torch.randn(n, dtype=torch.float64, device=dev, generator=gen),
+          "p": torch.zeros(n, dtype=torch.float64, device=dev),
+          "e": torch.rand(n, dtype=torch.float64, device=dev, generator=gen),
+          "m": torch.full((n,), 1.0 * ds ** dim, dtype=torch.float64, device=dev)}
+    cfg = dict(dt=1e-5, c_sound=10.0, rho0=1.0, mu=1e-3, body_force=(0.0, -1.0, 0.0)[:dim],
+               evolve_density=True, compute_energy=True)
+    per_row = 24 if dim == 2 else 80
+    off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    nb = torch.empty(per_row * n, dtype=torch.int32, device=dev)
+
+    # parity: one step from a copy of the initial state against the reference
+    parity = {"checked": False}
+    cpu = None
+    if os.path.exists(O.REF_SO):
+        lib = O.ref_lib()
+        lib.ref_set_threads(os.cpu_count() or 1)
+        xh = [a.cpu().numpy() for a in xd]
+        rs = O.RefSystem.from_arrays(xh, ds, h=h)
+        ref = O.RefMixed(rs, (0, 0, 0), 2)
+        for k in range(dim):
+            ref.set("v", k, st["v"][k].cpu().numpy())
+        ref.set("rho", 0, st["rho"].cpu().numpy())
+        ref.set("e", 0, st["e"].cpu().numpy())
+        t0 = time.perf_counter()
+        want_mx, want_tot = ref.step(**cfg)
+        t_ref = time.perf_counter() - t0
+        cp = {k: ([a.clone() for a in v] if isinstance(v, list) else
+                  (v.clone() if hasattr(v, "clone") else v)) for k, v in st.items()}
+        mx, tot = ctx.step_mixed_device(grid, 2, cp, cfg, off, nb)
+        torch.cuda.synchronize()
+        woff, wit = ref.table(want_tot)
+        ok = tot == want_tot and mx == want_mx and np.array_equal(off.cpu().numpy(), woff)
+        ok = ok and np.array_equal(nb[:tot].cpu().numpy(), wit)
+        for name in ("x", "v", "rel", "cell"):
+            ok = ok and all(np.array_equal(cp[name][k].cpu().numpy(), ref.get(name, k))
+                            for k in range(dim))
+        for name in ("rho", "p", "e"):
+            ok = ok and np.array_equal(cp[name].cpu().numpy(), ref.get(name))
+        c_of, c_st, c_it = ref.grid_members(C)
+        ok = ok and np.array_equal(cp["items"].cpu().numpy(), c_it)
+        ok = ok and np.array_equal(cp["cell_start"].cpu().numpy(), c_st)
+        parity = {"checked": True, "bit_exact_vs_reference_step_mixed": bool(ok),
+                  "fields": "table, max_dx, x, v, rho, p, e, RelCoords, grid membership"}
+        cpu = {"value": n / t_ref, "unit": "particles/s", "cores": int(lib.ref_max_threads()),
+               "kind": "reference",
+               "sample": "one full step_mixed (approach III) on the same state, all host threads"}
+        del cp
+
+    def step():
+        return ctx.step_mixed_device(grid, 2, st, cfg, off, nb)
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    launches0 = ctx.launches
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    t = statistics.mean(a.elapsed_time(b) for a, b in ev) * 1e-3
+    total = int(off[n].item())
+    # algorithmic bytes: the NNPS step's + the FP64 state (x, v, m, rho, p, e read,
+    # x, v, rho, p, e, rel written) + the table read twice (stress, rates)
+    s_pos = 2 * dim
+    b_nnps = n * s_pos + 4 * n + 4 * (C + 1) + 8 * (n + 1) + 4 * total
+    b_state = 8 * n * (2 * dim + 4) + 8 * n * (2 * dim + 3) + 8 * n * dim
+    b_table = 2 * (8 * (n + 1) + 4 * total)
+    b = b_nnps + b_state + b_table
+    peak, peak_kind = measured_peaks()
+    line = {
+        "metric": "mixed time step particles/s", "value": n / t, "unit": "particles/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f16 search, f64 rates", "data": "synthetic",
+        "config": {"workload": w["desc"] + " + step_mixed approach III (SURVEY 8(f) row 3)",
+                   "n_particles": n, "table_entries": total, "l2": "flushed between timed steps"},
+        "parity": parity,
+        "roofline": {"bound": "hbm", "kernel": "whole step", "achieved": b / t / 1e9,
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": b / t / 1e9 / peak, "algorithmic_bytes": b,
+                     "note": "the FP64 rates (divisions and square roots per pair) dominate"},
+        "gpu_launches": ctx.launches - launches0,
+        "clocks": clk.summary(),
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
 
 

@@ -953,7 +953,7 @@ int sphx_step_mixed_device(sphx_context* ctx, const sphx_grid_desc* grid, int32_
   a.off = d_offsets;
   a.nb = d_items_out;
   TRY(ctx->s_stress.ensure(sizeof(double) * 18 * n));
-  TRY(ctx->s_rates.ensure(sizeof(double) * 5 * n));
+  TRY(ctx->s_rates.ensure(sizeof(double) * 6 * n));
   TRY(ctx->s_dx.ensure(sizeof(double) * 3 * n));
   TRY(ctx->s_flags.ensure(2 * sizeof(unsigned long long)));
   double* sb = ctx->s_stress.as<double>();
@@ -965,6 +965,7 @@ int sphx_step_mixed_device(sphx_context* ctx, const sphx_grid_desc* grid, int32_
   }
   a.drho = rb;
   a.de = rb + n;
+  a.inv_r2 = rb + (size_t)5 * n;
   for (int k = 0; k < 3; ++k) {
     a.x[k] = k < dim ? state->x[k] : nullptr;
     a.v[k] = k < dim ? state->v[k] : nullptr;

@@ -187,6 +187,7 @@ struct StepArgs {
   double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0}, span[3] = {0, 0, 0};
   int per[3] = {0, 0, 0};
   unsigned long long* maxdx = nullptr;  // bits of the non-negative max |dx|
+  double* inv_r2 = nullptr;  // 1 / (rho rho) per particle (rhs_momentum / rhs_energy)
 };
 
 }  // namespace sphx_dev

@@ -48,10 +48,15 @@ __device__ __forceinline__ void kgrad(const double (&dx)[3], double h, double al
   for (int k = 0; k < D; ++k) gw[k] = __dmul_rn(sc, dx[k]);
 }
 
+// apply_eos, and 1/(rho rho) once per particle: rhs_momentum / rhs_energy evaluate
+// the same expression for every pair (dynamics.cpp:74, :79, :103, :108)
 __global__ void k_eos(int64_t n, const double* __restrict__ rho, double* __restrict__ p, double c2,
-                      double rho0) {
+                      double rho0, double* __restrict__ inv_r2) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) p[i] = __dmul_rn(c2, __dsub_rn(rho[i], rho0));
+  if (i >= n) return;
+  const double r = rho[i];
+  p[i] = __dmul_rn(c2, __dsub_rn(r, rho0));
+  inv_r2[i] = __ddiv_rn(1.0, __dmul_rn(r, r));
 }
 
 template <int D>
@@ -120,7 +125,7 @@ __global__ void __launch_bounds__(128) k_rates(StepArgs a) {
 #pragma unroll
     for (int b = c; b < D; ++b) si[sym(c, b)] = a.sig[sym(c, b)][i];
   const double rhoi = a.rho[i], pi = a.p[i];
-  const double inv_i = __ddiv_rn(1.0, __dmul_rn(rhoi, rhoi));
+  const double inv_i = a.inv_r2[i];
   double acc_rho = 0.0, acc_e = 0.0, acc_v[3] = {0.0, 0.0, 0.0};
   const int64_t e0 = a.off[i], e1 = a.off[i + 1];
   for (int64_t q = e0; q < e1; ++q) {
@@ -135,8 +140,7 @@ __global__ void __launch_bounds__(128) k_rates(StepArgs a) {
     for (int k = 0; k < D; ++k)
       dv_dot = __dadd_rn(dv_dot, __dmul_rn(__dsub_rn(vi[k], __ldg(a.v[k] + j)), gw[k]));
     acc_rho = __dadd_rn(acc_rho, __dmul_rn(mj, dv_dot));
-    const double rhoj = __ldg(a.rho + j);
-    const double inv_j = __ddiv_rn(1.0, __dmul_rn(rhoj, rhoj));
+    const double inv_j = __ldg(a.inv_r2 + j);
 #pragma unroll
     for (int c = 0; c < D; ++c) {  // rhs_momentum
       double term = 0.0;
@@ -173,35 +177,45 @@ __global__ void __launch_bounds__(128) k_rates(StepArgs a) {
 }
 
 template <int D>
-__global__ void k_kick_drift(StepArgs a) {
+__global__ void __launch_bounds__(256) k_kick_drift(StepArgs a) {
+  __shared__ double wmax[8];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.n_mov) return;
-#pragma unroll
-  for (int k = 0; k < D; ++k) a.v[k][i] = __dadd_rn(a.v[k][i], __dmul_rn(a.dv[k][i], a.dt));
-  if (a.evolve_density) a.rho[i] = __dadd_rn(a.rho[i], __dmul_rn(a.drho[i], a.dt));
-  if (a.compute_energy) a.e[i] = __dadd_rn(a.e[i], __dmul_rn(a.de[i], a.dt));
   double mx = 0.0;
+  if (i < a.n_mov) {
 #pragma unroll
-  for (int k = 0; k < D; ++k) {
-    const double d = __dmul_rn(a.v[k][i], a.dt);
-    mx = fmax(mx, fabs(d));
-    double xk = __dadd_rn(a.x[k][i], d);
-    if (a.per[k]) {
-      if (xk >= a.hi[k]) xk = __dsub_rn(xk, a.span[k]);
-      if (xk < a.lo[k]) xk = __dadd_rn(xk, a.span[k]);
+    for (int k = 0; k < D; ++k) a.v[k][i] = __dadd_rn(a.v[k][i], __dmul_rn(a.dv[k][i], a.dt));
+    if (a.evolve_density) a.rho[i] = __dadd_rn(a.rho[i], __dmul_rn(a.drho[i], a.dt));
+    if (a.compute_energy) a.e[i] = __dadd_rn(a.e[i], __dmul_rn(a.de[i], a.dt));
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const double d = __dmul_rn(a.v[k][i], a.dt);
+      mx = fmax(mx, fabs(d));
+      double xk = __dadd_rn(a.x[k][i], d);
+      if (a.per[k]) {
+        if (xk >= a.hi[k]) xk = __dsub_rn(xk, a.span[k]);
+        if (xk < a.lo[k]) xk = __dadd_rn(xk, a.span[k]);
+      }
+      a.x[k][i] = xk;
+      a.dx[k][i] = d;
     }
-    a.x[k][i] = xk;
-    a.dx[k][i] = d;
   }
-  // |dx| >= 0: the IEEE bit pattern orders like the value
-  atomicMax(a.maxdx, (unsigned long long)__double_as_longlong(mx));
+  // max |dx| over the block, then one atomic per block (|dx| >= 0: the IEEE bit
+  // pattern orders like the value)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, wmax[w]);
+    atomicMax(a.maxdx, (unsigned long long)__double_as_longlong(mx));
+  }
 }
 
 // Launches the rates part of the step on `st`; returns the number of kernels.
 int launch_step_rates(int dim, const StepArgs& a, cudaStream_t st) {
   if (a.n == 0) return 0;
   const unsigned g256 = (unsigned)((a.n + 255) / 256), g128 = (unsigned)((a.n + 127) / 128);
-  k_eos<<<g256, 256, 0, st>>>(a.n, a.rho, a.p, a.c2, a.rho0);
+  k_eos<<<g256, 256, 0, st>>>(a.n, a.rho, a.p, a.c2, a.rho0, a.inv_r2);
 #define RATES(D)                              \
   if (dim == D) {                             \
     k_stress<D><<<g128, 128, 0, st>>>(a);     \
