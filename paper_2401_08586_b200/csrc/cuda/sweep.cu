@@ -989,9 +989,9 @@ template <int D>
 struct R16Two {
   static constexpr int W = D == 3 ? 16 : 4;          // hit words per row
   static constexpr int TB = 256, TMINB = D == 3 ? 4 : 5;   // test kernel: threads, CTAs/SM
-  static constexpr int BT = D == 3 ? 64 : 128;       // emit kernel tile
-  static constexpr int PCAP = D == 3 ? 64 * 60 : 128 * 20;
-  static constexpr int EMINB = D == 3 ? 12 : 10;
+  static constexpr int BT = 128;                      // emit kernel tile
+  static constexpr int PCAP = D == 3 ? 128 * 60 : 128 * 20;
+  static constexpr int EMINB = D == 3 ? 7 : 10;
 };
 
 // the row's run in each (dz, dy) slot q (empty: cb == ce), RCLL cell of particle i
