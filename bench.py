@@ -62,6 +62,9 @@ def parse():
                     help="table: the NNPS table (default); grad: fused FP16 RCLL -> "
                          "grad_normalized (SURVEY 8(f) row 1), no table in HBM; step: the "
                          "mixed time step step_mixed, approach III (SURVEY 8(f) row 3)")
+    ap.add_argument("--order", default="lattice", choices=["lattice", "shuffled", "sorted"],
+                    help="particle numbering (SURVEY 8(d) locality study): the generator's "
+                         "lattice order, a seeded random shuffle, or cell-major order")
     ap.add_argument("--slab", action="store_true",
                     help="use the slab-decomposed (multi-GPU) path even at N=1")
     return ap.parse_args()
@@ -301,6 +304,54 @@ def sampled_parity(config, w, grid, prec, rel, cell, start, items, offsets, out,
 # ---------------------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------------------
+def renumber(args, ctx, grid, prec, xd, rel, cell, cell_of, start, items, dim):
+    """Renumber the particles (SURVEY 8(d) locality study) in place: a seeded random
+    shuffle or cell-major order (the binning's own CSR order). Returns the
+    permutation (new k holds old particle perm[k]) and the lattice-order table,
+    checked against the reference's golden hash, for the parity of the timed run."""
+    import torch
+
+    import paper_2401_08586_b200 as P
+    dev = xd[0].device
+    n = xd[0].numel()
+    off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    out = torch.empty(n * (24 if dim == 2 else 60), dtype=torch.int32, device=dev)
+    ctx.rcll_device(grid, rel, cell, items, start, prec, off, out)
+    torch.cuda.synchronize()
+    total = int(off[-1])
+    g_off, g_it = off.cpu().numpy(), out[:total].cpu().numpy()
+    g_ok = False
+    if args.config in ("C1", "C2", "C3"):
+        gold = golden(args.config, args.precision)
+        g_ok = total == gold["total"] and f"{P.capi.table_hash(g_off, g_it):016x}" == gold["hash"]
+    if args.order == "shuffled":
+        perm = np.random.default_rng(12345).permutation(n).astype(np.int64)
+    else:
+        perm = items.cpu().numpy().astype(np.int64)
+    pt = torch.from_numpy(perm).to(dev)
+    for k in range(dim):
+        xd[k].copy_(xd[k][pt])
+    ctx.build_rel_coords_device(grid, xd, rel, cell, cell_of, start, items)
+    return perm, g_off, g_it, g_ok
+
+
+def renumber_table(off, it, perm):
+    """The table of the renumbered system: row k is old row perm[k] with every id j
+    replaced by inv[j], re-sorted."""
+    n = len(perm)
+    inv = np.empty(n, np.int64)
+    inv[perm] = np.arange(n)
+    lens = np.diff(off)[perm]
+    new_off = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=new_off[1:])
+    total = int(new_off[-1])
+    src = np.repeat(off[:-1][perm] - new_off[:-1], lens) + np.arange(total)
+    vals = inv[it[src]]
+    rows = np.repeat(np.arange(n), lens)
+    order = np.lexsort((vals, rows))
+    return new_off, vals[order].astype(np.int32)
+
+
 def run_ours(args):
     import torch
 
@@ -344,6 +395,9 @@ def run_ours(args):
     start = torch.empty(C + 1, dtype=torch.int32, device=dev)
     items = torch.empty(n, dtype=torch.int32, device=dev)
     ctx.build_rel_coords_device(grid, xd, rel, cell, cell_of, start, items)
+    reorder = None
+    if args.order != "lattice" and args.op == "table" and not w.get("device_lattice"):
+        reorder = renumber(args, ctx, grid, prec, xd, rel, cell, cell_of, start, items, dim)
     if args.op == "grad":
         return bench_grad(args, w, ctx, stream, grid, n, C, xd, rel, cell, items, start, local)
     if args.op == "step":
@@ -418,7 +472,16 @@ def run_ours(args):
             assert tot == total
 
     # ---- parity of the timed output -------------------------------------------------------
-    if args.config in ("C1", "C2", "C3"):  # the reference's golden table hash
+    if reorder is not None:  # the golden lattice-order table, renumbered
+        perm, g_off, g_it, g_ok = reorder
+        w_off, w_it = renumber_table(g_off, g_it, perm)
+        same = (np.array_equal(offsets.cpu().numpy(), w_off)
+                and np.array_equal(out[:total].cpu().numpy(), w_it))
+        parity = {"bit_exact_vs_reference_hash": bool(g_ok and same),
+                  "method": f"lattice-order table (golden hash {'ok' if g_ok else 'FAILED'}) "
+                            f"renumbered to the {args.order} order, rows re-sorted, compared "
+                            "entry for entry"}
+    elif args.config in ("C1", "C2", "C3"):  # the reference's golden table hash
         gold = golden(args.config, args.precision)
         dev_hash = P.capi.table_hash(offsets.cpu().numpy(), out[:total].cpu().numpy())
         e2e_hash = P.capi.table_hash(h_off.numpy(), h_out.numpy()) if h_out is not None else dev_hash
@@ -451,6 +514,7 @@ def run_ours(args):
         "config": {"workload": w["desc"], "n_particles": n, "cells": C, "pairs": total,
                    "precision": args.precision, "backend": "rcll",
                    "input": "device-resident RelCoords (fp64) + CellGrid CSR",
+                   "order": args.order,
                    "l2": "flushed between timed steps (256 MiB write, outside the events)"},
         "parity": parity,
         "breakdown_ms": {"encode": statistics.mean(encode_ms), "sweep": t_sweep * 1e3,

@@ -439,6 +439,8 @@ def _oracle_lib():
             "so_f16_to_f64": (C.c_double, [C.c_uint16]),
             "so_round_to": (C.c_double, [C.c_int, C.c_double]),
             "so_lattice_count": (C.c_int64, [C.c_int, d3, d3, C.c_double]),
+            "so_build_gapped_random": (C.c_int, [d3, d3, C.c_int64, C.c_double, C.c_double,
+                                                 C.c_uint64, vp, vp]),
             "so_build_lattice": (C.c_int, [C.c_int, d3, d3, C.c_double, C.c_double, C.c_uint64,
                                            vp, vp, vp]),
             "so_build_random": (C.c_double, [C.c_int, d3, d3, C.c_int64, C.c_uint64, vp, vp, vp]),
@@ -505,6 +507,15 @@ class Oracle:
                                        *([x.ctypes.data for x in xs] + [None] * (3 - dim)))
         if rc != 0:
             raise ValueError("invalid lattice parameters")
+        return xs
+
+    def gapped_random(self, n, cutoff, width, seed, lo=(0, 0, 0), hi=(1, 1, 1)):
+        """build_gapped_random (experiments.cpp:55-112) positions, 2-D."""
+        xs = [np.empty(n, np.float64) for _ in range(2)]
+        rc = self.lib.so_build_gapped_random(_d3(lo), _d3(hi), n, cutoff, width, seed,
+                                             xs[0].ctypes.data, xs[1].ctypes.data)
+        if rc != 0:
+            raise RuntimeError("guard-annulus sampling stalled; widen the budget")
         return xs
 
     def random(self, dim, n, seed, lo=(0, 0, 0), hi=(1, 1, 1)):

@@ -103,6 +103,42 @@ uint64_t so_rng_below(so_rng* r, uint64_t n) {
 }
 
 /* ------------------------------------------------------------------------ */
+/* build_gapped_random (experiments.cpp:55-112), restated by brute force: a    */
+/* draw is rejected when any placed particle lies at squared distance in      */
+/* (lo2, hi2). The reference searches only the 3x3 buckets of edge            */
+/* cutoff + width around the draw; every particle closer than cutoff + width  */
+/* lies in them, so scanning all placed particles takes the same decisions.   */
+/* Returns 0, or -4 (the reference's runtime_error) after 4000 rejections.    */
+/* ------------------------------------------------------------------------ */
+int so_build_gapped_random(const double* lo, const double* hi, int64_t n, double cutoff,
+                           double width, uint64_t seed, double* x0, double* x1) {
+  so_rng rng;
+  so_rng_seed(&rng, seed);
+  const double lo2 = (cutoff - width) * (cutoff - width);
+  const double hi2 = (cutoff + width) * (cutoff + width);
+  for (int64_t i = 0; i < n; ++i) {
+    int attempt = 0;
+    for (;; ++attempt) {
+      if (attempt > 4000) return -4;
+      const double x = lo[0] + (hi[0] - lo[0]) * so_rng_uniform01(&rng); /* rng.hpp:17 */
+      const double y = lo[1] + (hi[1] - lo[1]) * so_rng_uniform01(&rng);
+      int ok = 1;
+      for (int64_t j = 0; j < i && ok; ++j) {
+        const double dx = x - x0[j], dy = y - x1[j];
+        const double d2 = dx * dx + dy * dy;
+        if (d2 > lo2 && d2 < hi2) ok = 0;
+      }
+      if (ok) {
+        x0[i] = x;
+        x1[i] = y;
+        break;
+      }
+    }
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Generators: particle_system.cpp:31-62 (lattice), :64-77 (uniform).        */
 /* ------------------------------------------------------------------------ */
 int64_t so_lattice_count(int dim, const double* lo, const double* hi, double ds) {

@@ -47,6 +47,10 @@ int so_build_lattice(int dim, const double* lo, const double* hi, double ds, dou
 double so_build_random(int dim, const double* lo, const double* hi, int64_t n, uint64_t seed,
                        double* x0, double* x1, double* x2);
 
+/* build_gapped_random (experiments.cpp:55-112), 2-D: 0 or -4 (stalled). */
+int so_build_gapped_random(const double* lo, const double* hi, int64_t n, double cutoff,
+                           double width, uint64_t seed, double* x0, double* x1);
+
 /* Uniform cell grid (cell_grid.cpp:9-34). */
 typedef struct so_grid {
   int dim;

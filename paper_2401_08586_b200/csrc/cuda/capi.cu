@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "sphx/binary16.hpp"
@@ -1237,6 +1238,66 @@ int sphx_build_lattice(int32_t dim, const double lo[3], const double hi[3], doub
         }
         ++idx;
       }
+  return SPHX_OK;
+}
+
+int sphx_build_gapped_random(const double lo[3], const double hi[3], int64_t n, double cutoff,
+                             double width, uint64_t seed, double* ds_out, double* x0, double* x1) {
+  // build_gapped_random (experiments.cpp:55-112): 2-D dart throwing with rejection;
+  // a candidate is redrawn while any placed particle lies at a distance within
+  // (cutoff - width, cutoff + width), searched over a bucket grid of edge
+  // cutoff + width. Sequential by construction (each draw depends on all earlier ones).
+  if (!ds_out || !lo || !hi) return fail(SPHX_ERR_INVALID_ARGUMENT, "null argument");
+  for (int k = 0; k < 2; ++k)
+    if (!(lo[k] < hi[k])) return fail(SPHX_ERR_INVALID_ARGUMENT, "domain bounds must satisfy lo < hi");
+  if (n <= 0) return fail(SPHX_ERR_INVALID_ARGUMENT, "particle count must be positive");
+  const double span0 = hi[0] - lo[0], span1 = hi[1] - lo[1];
+  *ds_out = std::pow(span0 * span1 / static_cast<double>(n), 0.5);  // ParticleSystem ds
+  if (!x0 || !x1) return SPHX_OK;
+  std::mt19937_64 gen(seed);
+  auto uniform = [&](double a, double b) {  // rng.hpp:15-17
+    return a + (b - a) * (static_cast<double>(gen() >> 11) * 0x1.0p-53);
+  };
+  const double lo2 = (cutoff - width) * (cutoff - width);
+  const double hi2 = (cutoff + width) * (cutoff + width);
+  const double bucket = cutoff + width;
+  const int bx = std::max(1, static_cast<int>(span0 / bucket));
+  const int by = std::max(1, static_cast<int>(span1 / bucket));
+  std::vector<std::vector<int32_t>> cells(static_cast<size_t>(bx) * by);
+  auto cell_of = [&](double x, double y, int& cx, int& cy) {
+    cx = std::min(std::max(static_cast<int>((x - lo[0]) / span0 * bx), 0), bx - 1);
+    cy = std::min(std::max(static_cast<int>((y - lo[1]) / span1 * by), 0), by - 1);
+  };
+  for (int64_t i = 0; i < n; ++i) {
+    for (int attempt = 0;; ++attempt) {
+      if (attempt > 4000)
+        return fail(SPHX_ERR_RUNTIME, "guard-annulus sampling stalled; widen the budget");
+      const double x = uniform(lo[0], hi[0]);
+      const double y = uniform(lo[1], hi[1]);
+      int cx, cy;
+      cell_of(x, y, cx, cy);
+      bool ok = true;
+      for (int oy = -1; oy <= 1 && ok; ++oy)
+        for (int ox = -1; ox <= 1 && ok; ++ox) {
+          const int qx = cx + ox, qy = cy + oy;
+          if (qx < 0 || qy < 0 || qx >= bx || qy >= by) continue;
+          for (const int32_t j : cells[static_cast<size_t>(qy) * bx + qx]) {
+            const double dx = x - x0[j], dy = y - x1[j];
+            const double d2 = dx * dx + dy * dy;
+            if (d2 > lo2 && d2 < hi2) {
+              ok = false;
+              break;
+            }
+          }
+        }
+      if (ok) {
+        x0[i] = x;
+        x1[i] = y;
+        cells[static_cast<size_t>(cy) * bx + cx].push_back(static_cast<int32_t>(i));
+        break;
+      }
+    }
+  }
   return SPHX_OK;
 }
 
