@@ -1948,6 +1948,16 @@ __global__ void __launch_bounds__(XYShape::BT) k_encode_xy(EncArgs e, SweepArgs 
   const int64_t plane = (row - y) * nx;         // first cell of plane z
   const int nrun = x1 - x0;
 
+  // empty runs only (a run holds its own cell, so the CTA's cells are empty too):
+  // the chunk ranges are all that is written (dam-break C4: 3/4 of the grid)
+  {
+    const int64_t c0 = plane + (int64_t)y * nx + x0;
+    if (e.cstart[c0 + nrun] == e.cstart[c0]) {
+      for (int v = tid; v < nrun; v += BT) a.tri[c0 + v] = make_int2(e.cstart[c0], e.cstart[c0]);
+      return;
+    }
+  }
+
   // window cells: rows y-1, y, y+1 (r = 0, 1, 2), columns x0-2 .. x1+1
   if (tid < 32) {
     int tot = 0;
