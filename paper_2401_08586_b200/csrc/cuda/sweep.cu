@@ -229,12 +229,26 @@ struct ChunkLay {
   static constexpr int NQP = NQ <= 1 ? 1 : (NQ <= 2 ? 2 : 4);
   static constexpr int BYTES = QB * NQP;
 };
-// 3-D FP16 RCLL uses xy-plane runs (k_encode_xy): records {x, y, z, dcx, dcy}
-// quads, 40 bytes padded to 48 (three 16-byte loads).
+// 3-D FP16 RCLL uses xy-plane runs (k_encode_xy). A chunk is 32 bytes (one
+// 256-bit load): the x, y, z quads, then for each of dcx and dcy one word of PRMT
+// selector nibbles, (s1 << 12 | s0 << 4) per record pair, s = 0 / 1 / 2 for an
+// offset of 0 / +1 / -1 (dc_half2 turns a pair's selector into its half2).
 template <>
 struct ChunkLay<3, FP16, MODE_RCLL> {
-  static constexpr int QB = 8, NQ = 5, NQP = 6, BYTES = 48;
+  static constexpr int QB = 8, NQ = 3, NQP = 4, BYTES = 32;
+  static constexpr int SELX = 24, SELY = 28;  // byte offsets of the selector words
 };
+
+// selector nibble of record l (0..3) for a cell offset code s (0: 0, 1: +1, 2: -1)
+__device__ __forceinline__ uint32_t dc_nibble(int l, uint32_t s) {
+  return s << (16 * (l >> 1) + ((l & 1) ? 12 : 4));
+}
+
+// half2 {dc_l0, dc_l1} of a record pair from its 16 selector bits:
+// bytes 00 3C BC pick the high byte of 0, +1.0, -1.0
+__device__ __forceinline__ __half2 dc_half2(uint32_t sel16) {
+  return u2h(__byte_perm(0x00BC3C00u, 0u, sel16));
+}
 
 // element u (0..3) of quad q of chunk ch
 template <int D, int P, int MODE>
@@ -733,19 +747,22 @@ __device__ __forceinline__ void r16_chunk(const char* __restrict__ qc, int ch, c
                                           __half2 ccy, __half2 ccz, unsigned& acc) {
   __half2 a[2];
   if constexpr (D == 3) {
-    // xy-plane run record (48 B): x, y quads | z, dcx quads | dcy quad; ccy is the
-    // y cell edge (dcy per record), ccz the run's z centre difference
-    const uint4* p = reinterpret_cast<const uint4*>(qc + (size_t)ch * 48);
-    const uint4 v0 = __ldg(p), v1 = __ldg(p + 1);
-    const uint2 v2 = __ldg(reinterpret_cast<const uint2*>(p + 2));
+    // xy-plane run chunk (32 B, one 256-bit load): x, y | z quads, dcx, dcy
+    // selector words; ccy is the y cell edge (dcy per record), ccz the run's z
+    // centre difference
+    uint4 v0, v1;
+    asm("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(v0.x), "=r"(v0.y), "=r"(v0.z), "=r"(v0.w), "=r"(v1.x), "=r"(v1.y), "=r"(v1.z),
+          "=r"(v1.w)
+        : "l"(qc + (size_t)ch * 32));
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const unsigned xj = h ? v0.y : v0.x, yj = h ? v0.w : v0.z, zj = h ? v1.y : v1.x;
       __half2 t = __hmul2_rn(__hsub2_rn(r2[0], u2h(xj)), hh2[0]);
-      __half2 d = __hfma2(u2h(h ? v1.w : v1.z), hc2, t);
+      __half2 d = __hfma2(dc_half2(h ? v1.z >> 16 : v1.z), hc2, t);
       __half2 acc2 = __hmul2_rn(d, d);
       t = __hmul2_rn(__hsub2_rn(r2[1], u2h(yj)), hh2[1]);
-      d = __hfma2(u2h(h ? v2.y : v2.x), ccy, t);
+      d = __hfma2(dc_half2(h ? v1.w >> 16 : v1.w), ccy, t);
       acc2 = __hadd2_rn(acc2, __hmul2_rn(d, d));
       t = __hadd2_rn(__hmul2_rn(__hsub2_rn(r2[2], u2h(zj)), hh2[2]), ccz);
       acc2 = __hadd2_rn(acc2, __hmul2_rn(t, t));
@@ -1918,7 +1935,8 @@ struct XYShape {
 };
 
 constexpr size_t xy_smem_bytes() {
-  return (size_t)XYShape::WCAP * (4 + 4 + 4 + 2 + 1) + (size_t)XYShape::OCAP * (48 + 16);
+  return (size_t)XYShape::WCAP * (4 + 4 + 4 + 2 + 1) +
+         (size_t)XYShape::OCAP * (ChunkLay<3, FP16, MODE_RCLL>::BYTES + 16);
 }
 
 __global__ void __launch_bounds__(XYShape::BT) k_encode_xy(EncArgs e, SweepArgs a) {
@@ -2032,14 +2050,13 @@ __global__ void __launch_bounds__(XYShape::BT) k_encode_xy(EncArgs e, SweepArgs 
   const int nch = s_nch;
   const bool out_sm = nch <= S::OCAP;
   const __half nanv = hbits(0x7E00u);
-  if (out_sm) {
-    for (int q = tid; q < nch * 4; q += BT) {
-      const int c = q >> 2, l = q & 3;
-#pragma unroll
-      for (int k = 0; k < 3; ++k) *rec_el<3, FP16, MODE_RCLL>(sch, c, k, l) = nanv;
-      *rec_el<3, FP16, MODE_RCLL>(sch, c, 3, l) = hbits(0);
-      *rec_el<3, FP16, MODE_RCLL>(sch, c, 4, l) = hbits(0);
-      stag[q] = 0xFFFFFFFFu;
+  if (out_sm) {  // NaN coordinates, zero selectors, ~0 ids
+    const uint32_t nan2 = 0x7E007E00u;
+    for (int c = tid; c < nch; c += BT) {
+      uint4* ck = reinterpret_cast<uint4*>(sch + (size_t)c * L::BYTES);
+      ck[0] = make_uint4(nan2, nan2, nan2, nan2);
+      ck[1] = make_uint4(nan2, nan2, 0u, 0u);
+      reinterpret_cast<uint4*>(stag)[c] = make_uint4(~0u, ~0u, ~0u, ~0u);
     }
   } else {
     for (int v = tid; v < nrun; v += BT) {  // pad records of each run
@@ -2051,10 +2068,11 @@ __global__ void __launch_bounds__(XYShape::BT) k_encode_xy(EncArgs e, SweepArgs 
       for (int64_t q = r0 + len; q < r1; ++q) {
 #pragma unroll
         for (int k = 0; k < 3; ++k) store_el<3, FP16, MODE_RCLL>(a.qc, q, k, nanv);
-        store_el<3, FP16, MODE_RCLL>(a.qc, q, 3, hbits(0));
-        store_el<3, FP16, MODE_RCLL>(a.qc, q, 4, hbits(0));
         reinterpret_cast<unsigned*>(a.qtag)[q] = 0xFFFFFFFFu;
       }
+      for (int64_t ch = r0 >> 2; ch < (r1 >> 2); ++ch)  // selectors are OR-ed in below
+        *reinterpret_cast<uint2*>(static_cast<char*>(a.qc) + ch * L::BYTES + L::SELX) =
+            make_uint2(0u, 0u);
     }
   }
 
@@ -2093,21 +2111,24 @@ __global__ void __launch_bounds__(XYShape::BT) k_encode_xy(EncArgs e, SweepArgs 
       const int pos = col[1 + dv] + col[2 + dv] + col[3 + dv];
       const int64_t cidx = plane + (int64_t)y * nx + (x0 + v - 2);
       const int64_t rec = 4 * (int64_t)e.cstart[cidx] + pos;
-      const __half dcx = hbits(dv == 1 ? 0x3C00u : (dv == -1 ? 0xBC00u : 0u));  // v - u
-      const __half dcy = hbits(r == 0 ? 0x3C00u : (r == 2 ? 0xBC00u : 0u));    // 1 - r
+      const uint32_t sx = dv == 1 ? 1u : (dv == -1 ? 2u : 0u);  // dcx = v - u
+      const uint32_t sy = r == 0 ? 1u : (r == 2 ? 2u : 0u);     // dcy = 1 - r
       const uint32_t tag = a.ids ? (uint32_t)key : (uint32_t)j;
+      const int l = (int)(rec & 3);
       if (out_sm) {
         const int lr = (int)(rec - 4 * ch0);
 #pragma unroll
-        for (int k = 0; k < 3; ++k) *rec_el<3, FP16, MODE_RCLL>(sch, lr >> 2, k, lr & 3) = c[k];
-        *rec_el<3, FP16, MODE_RCLL>(sch, lr >> 2, 3, lr & 3) = dcx;
-        *rec_el<3, FP16, MODE_RCLL>(sch, lr >> 2, 4, lr & 3) = dcy;
+        for (int k = 0; k < 3; ++k) *rec_el<3, FP16, MODE_RCLL>(sch, lr >> 2, k, l) = c[k];
+        unsigned char* ck = sch + (size_t)(lr >> 2) * L::BYTES;
+        if (sx) atomicOr(reinterpret_cast<unsigned*>(ck + L::SELX), dc_nibble(l, sx));
+        if (sy) atomicOr(reinterpret_cast<unsigned*>(ck + L::SELY), dc_nibble(l, sy));
         stag[lr] = tag;
       } else {
 #pragma unroll
         for (int k = 0; k < 3; ++k) store_el<3, FP16, MODE_RCLL>(a.qc, rec, k, c[k]);
-        store_el<3, FP16, MODE_RCLL>(a.qc, rec, 3, dcx);
-        store_el<3, FP16, MODE_RCLL>(a.qc, rec, 4, dcy);
+        char* ck = static_cast<char*>(a.qc) + (rec >> 2) * L::BYTES;
+        if (sx) atomicOr(reinterpret_cast<unsigned*>(ck + L::SELX), dc_nibble(l, sx));
+        if (sy) atomicOr(reinterpret_cast<unsigned*>(ck + L::SELY), dc_nibble(l, sy));
         reinterpret_cast<uint32_t*>(a.qtag)[rec] = tag;
       }
       if (dv == 0 && r == 1) {  // own cell: pos_own and the self record
@@ -2193,7 +2214,7 @@ __global__ void __launch_bounds__(XYShape::BT) k_encode_xy(EncArgs e, SweepArgs 
   if (out_sm) {
     const uint4* src = reinterpret_cast<const uint4*>(sch);
     uint4* dst = reinterpret_cast<uint4*>(static_cast<char*>(a.qc) + ch0 * L::BYTES);
-    for (int q = tid; q < nch * 3; q += BT) dst[q] = src[q];
+    for (int q = tid; q < nch * (L::BYTES / 16); q += BT) dst[q] = src[q];
     const uint4* ts = reinterpret_cast<const uint4*>(stag);
     uint4* td = reinterpret_cast<uint4*>(a.qtag) + ch0;
     for (int q = tid; q < nch; q += BT) td[q] = ts[q];
