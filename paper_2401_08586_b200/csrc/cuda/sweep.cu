@@ -2012,13 +2012,13 @@ __global__ void __launch_bounds__(XYShape::BT) k_encode_xy(EncArgs e, SweepArgs 
   const int W = wst[NWC];
   const bool win_sm = W <= S::WCAP;
 
-  auto find_cell = [&](int m) {  // last w with wst[w] <= m
-    int lo = 0, hi = NWC;
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (wst[mid] <= m) lo = mid; else hi = mid;
-    }
-    return lo;
+  auto find_cell = [&](int m) {  // last w with wst[w] <= m (binary lifting, NWC < 64)
+    static_assert(NWC < 64, "window cells");
+    int w = 0;
+#pragma unroll
+    for (int st = 32; st > 0; st >>= 1)
+      if (w + st < NWC && wst[w + st] <= m) w += st;
+    return w;
   };
   auto member_id = [&](int m, int w) { return __ldg(e.items + wgs[w] + (m - wst[w])); };
   if (win_sm) {
@@ -2079,6 +2079,13 @@ __global__ void __launch_bounds__(XYShape::BT) k_encode_xy(EncArgs e, SweepArgs 
   auto less_in = [&](int w, int key) {  // keys below `key` in window cell w (lower bound)
     const int lo = wst[w];
     int base = lo, len = wst[w + 1] - lo;
+    if (win_sm && len < 32) {  // branch-free binary lifting
+      int b = 0;
+#pragma unroll
+      for (int st = 16; st > 0; st >>= 1)
+        if (b + st <= len && skey[lo + b + st - 1] < key) b += st;
+      return b;
+    }
     if (win_sm) {
       while (len > 0) {
         const int half = len >> 1;
