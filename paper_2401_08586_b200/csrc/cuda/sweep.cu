@@ -1700,14 +1700,17 @@ __global__ void __launch_bounds__(EncShape<D, P>::BT) k_encode_rows(EncArgs e, S
   const bool win_sm = W <= E::WCAP;
 
   // member window: key, id, coordinates
+  auto cell_of_member = [&](int m) {  // last u with wst[u] <= m (binary lifting)
+    static_assert(NW < 128, "window cells");
+    int w = 0;
+#pragma unroll
+    for (int st = 64; st > 0; st >>= 1)
+      if (w + st < NW && wst[w + st] <= m) w += st;
+    return w;
+  };
   auto member = [&](int m, int& u) {
-    int lo = 0, hi = NW;  // last u with wst[u] <= m
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (wst[mid] <= m) lo = mid; else hi = mid;
-    }
-    u = lo;
-    return __ldg(e.items + wgs[lo] + (m - wst[lo]));
+    u = cell_of_member(m);
+    return __ldg(e.items + wgs[u] + (m - wst[u]));
   };
   if (win_sm) {
     for (int m = tid; m < W; m += BT) {
@@ -1797,11 +1800,7 @@ __global__ void __launch_bounds__(EncShape<D, P>::BT) k_encode_rows(EncArgs e, S
   // records: members of window cells 1 .. XB+2 (x0-1 .. x1)
   const int mlo = wst[1], mhi = wst[min(x1 - x0 + 3, NW)];
   for (int m = mlo + tid; m < mhi; m += BT) {
-    int u = 1, hi = NW;  // last u with wst[u] <= m
-    while (hi - u > 1) {
-      const int mid = (u + hi) >> 1;
-      if (wst[mid] <= m) u = mid; else hi = mid;
-    }
+    const int u = cell_of_member(m);  // >= 1: m >= wst[1]
     const int idx = m - wst[u];
     const int key = key_of(m), j = id_of(m);
     T c[3];
