@@ -369,7 +369,7 @@ def run_ours(args):
     if world > 1 or args.slab:
         from paper_2401_08586_b200 import multigpu
         return multigpu.bench(args, WORKLOADS, METRIC, clock_sampler=ClockSampler,
-                              peaks=measured_peaks())
+                              peaks=measured_peaks(), golden=golden)
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -743,6 +743,12 @@ def bench_step(args, w, ctx, stream, grid, n, C, xd, rel, cell, cell_of, items, 
 
 
 def main():
+    # rank 0's stdout carries exactly one JSON line: keep NCCL's version banner
+    # (NCCL_DEBUG=VERSION in this image; NCCL prints it at WARN too) off it. NCCL
+    # reads the variable when torch first calls into it, so this precedes every
+    # torch import; NCCL_DEBUG=INFO/TRACE set by a user is left alone.
+    if os.environ.get("NCCL_DEBUG", "").upper() in ("VERSION", "WARN"):
+        del os.environ["NCCL_DEBUG"]
     args = parse()
     if args.impl == "reference":
         run_reference(args)

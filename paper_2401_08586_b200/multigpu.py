@@ -334,7 +334,7 @@ def _env():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def bench(args, workloads, metric, clock_sampler=None, peaks=(6650.0, "fallback")):
+def bench(args, workloads, metric, clock_sampler=None, peaks=(6650.0, "fallback"), golden=None):
     """Weak scaling: the config's lattice stacked `world` times along the slab axis
     (rank r owns about one config's worth of particles). A step is one rows() call
     per rank on resident slab inputs (owned + halo RelCoords + local CSR), the
@@ -454,6 +454,19 @@ def bench(args, workloads, metric, clock_sampler=None, peaks=(6650.0, "fallback"
     dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
     t_max, t_pipe, t_e2e = red.tolist()
     owned, pairs, launches_all, halo, h2d = [int(v) for v in cnt.tolist()]
+    # parity: one slab is the whole system, so its table must carry the reference's
+    # golden hash; with more slabs the stacked lattices have no reference table and
+    # tests/test_multigpu.py checks slab rows = one-GPU rows bit for bit
+    parity = {"checked": False,
+              "covered_by": "tests/test_multigpu.py (2/3/4 slabs, every precision: "
+                            "reassembled slab tables = the one-GPU table)"}
+    if world == 1 and golden is not None and args.config in ("C1", "C2", "C3"):
+        from .capi import table_hash
+        g = golden(args.config, args.precision)
+        h = table_hash(slab.offsets.cpu().numpy(), slab.out[:total].cpu().numpy())
+        parity = {"checked": True,
+                  "bit_exact_vs_reference_hash": total == g["total"] and f"{h:016x}" == g["hash"],
+                  "hash": f"{h:016x}", "golden": g["hash"]}
     if rank == 0:
         assert owned == n_global, (owned, n_global)
         t_sweep = statistics.mean(sweep_ms) * 1e-3
@@ -474,6 +487,7 @@ def bench(args, workloads, metric, clock_sampler=None, peaks=(6650.0, "fallback"
                        "precision": args.precision, "backend": "rcll",
                        "parallelism": f"slab{world} (cell layers along axis {plan.axis})",
                        "l2": "flushed between timed steps (256 MiB write, outside the events)"},
+            "parity": parity,
             "pipeline": {"ms_per_step": t_pipe * 1e3, "value": owned / t_pipe,
                          "what": "halo exchange (NCCL p2p) + window binning + rows"},
             "roofline": {"bound": "hbm", "kernel": "k_rcll16 (2-D) / k_r16_test + k_r16_emit (3-D), rank 0",
