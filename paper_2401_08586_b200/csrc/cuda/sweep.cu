@@ -740,8 +740,10 @@ struct R16 {
 };
 
 // One chunk (4 candidates) against particle i: the 4-bit hit nibble is shifted
-// into acc from the top (acc = acc >> 4 | nibble << 28).
-template <int D>
+// into acc from the top (acc = acc >> 4 | nibble << 28). ZC: the run's last
+// centre difference (z in 3-D, y in 2-D) is zero (the dz = 0 / dy = 0 run), so
+// its add is skipped: r16(t + 0) only turns -0 into +0, which is then squared.
+template <int D, bool ZC = false>
 __device__ __forceinline__ void r16_chunk(const char* __restrict__ qc, int ch, const __half2 (&r2)[3],
                                           const __half2 (&hh2)[3], __half2 hc2, __half2 thr2,
                                           __half2 ccy, __half2 ccz, unsigned& acc) {
@@ -764,7 +766,8 @@ __device__ __forceinline__ void r16_chunk(const char* __restrict__ qc, int ch, c
       t = __hmul2_rn(__hsub2_rn(r2[1], u2h(yj)), hh2[1]);
       d = __hfma2(dc_half2(h ? v1.w >> 16 : v1.w), ccy, t);
       acc2 = __hadd2_rn(acc2, __hmul2_rn(d, d));
-      t = __hadd2_rn(__hmul2_rn(__hsub2_rn(r2[2], u2h(zj)), hh2[2]), ccz);
+      t = __hmul2_rn(__hsub2_rn(r2[2], u2h(zj)), hh2[2]);
+      if constexpr (!ZC) t = __hadd2_rn(t, ccz);
       acc2 = __hadd2_rn(acc2, __hmul2_rn(t, t));
       a[h] = acc2;
     }
@@ -786,7 +789,8 @@ __device__ __forceinline__ void r16_chunk(const char* __restrict__ qc, int ch, c
       __half2 t = __hmul2_rn(__hsub2_rn(r2[0], u2h(xj)), hh2[0]);
       const __half2 d = __hfma2(u2h(h ? v1.y : v1.x), hc2, t);
       __half2 acc2 = __hmul2_rn(d, d);
-      t = __hadd2_rn(__hmul2_rn(__hsub2_rn(r2[1], u2h(yj)), hh2[1]), ccy);
+      t = __hmul2_rn(__hsub2_rn(r2[1], u2h(yj)), hh2[1]);
+      if constexpr (!ZC) t = __hadd2_rn(t, ccy);
       acc2 = __hadd2_rn(acc2, __hmul2_rn(t, t));
       a[h] = acc2;
     }
@@ -1074,7 +1078,7 @@ struct R16Own {
     unsigned acc = 0;
 #pragma unroll 4
     for (int ch = g; ch < e; ++ch) {
-      r16_chunk<D>(qc, ch, r2, hh2, hc2, thr2, ccy, ccz, acc);
+      r16_chunk<D, (Q == R16<D>::NR / 2)>(qc, ch, r2, hh2, hc2, thr2, ccy, ccz, acc);
       if (Q == R16<D>::NR / 2 && ch == selfch) acc &= selfmask;
     }
     return acc >> (4 * (8 - (e - g)));
