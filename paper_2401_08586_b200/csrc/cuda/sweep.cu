@@ -739,6 +739,29 @@ struct R16 {
   static constexpr int NR = 3;
 };
 
+// Programmatic dependent launch (sm_90+): the kernel may start while the previous
+// kernel on the stream finishes its last wave; it must execute
+// griddepcontrol.wait before reading that kernel's output (the previous kernel
+// executes griddepcontrol.launch_dependents at its start).
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block,
+                       cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 // One chunk (4 candidates) against particle i: the 4-bit hit nibble is shifted
 // into acc from the top (acc = acc >> 4 | nibble << 28). ZC: the run's last
 // centre difference (z in 3-D, y in 2-D) is zero (the dz = 0 / dy = 0 run), so
@@ -1098,6 +1121,8 @@ __device__ __forceinline__ void r16_for_slots(F&& f) {
 // coalesce and their loops run in step.
 template <int D>
 __global__ void __launch_bounds__(R16Two<D>::TB, R16Two<D>::TMINB) k_r16_test(SweepArgs a) {
+  pdl_trigger();  // the emit may launch once every test CTA has started
+  pdl_wait();     // the xy encode has completed
   constexpr int NR = R16<D>::NR, W = R16Two<D>::W;
   const int t = blockIdx.x * R16Two<D>::TB + threadIdx.x;
   if (t >= a.n) return;
@@ -1125,6 +1150,7 @@ __global__ void __launch_bounds__(R16Two<D>::TB, R16Two<D>::TMINB) k_r16_test(Sw
 template <int D, int BT, int PCAP>
 __global__ void __launch_bounds__(BT, BT == R16Two<D>::BT ? R16Two<D>::EMINB : R16Two<D>::EMINB_LARGE)
     k_r16_emit(SweepArgs a) {
+  pdl_wait();  // the tests have completed
   constexpr int NR = R16<D>::NR, W = R16Two<D>::W;
   __shared__ __align__(16) int32_t PK[PCAP + 4];
   __shared__ int s_w[BT / 32];
@@ -1272,6 +1298,7 @@ struct GradAcc {
 
 template <int D, int BT, int CAP, int W>
 __global__ void __launch_bounds__(BT) k_r16_grad(SweepArgs a) {
+  pdl_wait();  // the encode has completed
   constexpr int NR = R16<D>::NR;
   __shared__ __align__(16) int32_t ROWS[BT * CAP];
   __shared__ unsigned NIB[W * BT];
@@ -1367,12 +1394,14 @@ __global__ void __launch_bounds__(BT) k_r16_grad(SweepArgs a) {
 int launch_rcll_grad(int dim, const SweepArgs& a, cudaStream_t st) {
   if (dim == 2) {
     using G = R16Grad<2>;
-    k_r16_grad<2, G::BT, G::CAP, G::W><<<(unsigned)((a.n + G::BT - 1) / G::BT), G::BT, 0, st>>>(a);
+    launch_pdl(k_r16_grad<2, G::BT, G::CAP, G::W>, (unsigned)((a.n + G::BT - 1) / G::BT), G::BT,
+               st, a);
     return 1;
   }
   if (dim == 3) {
     using G = R16Grad<3>;
-    k_r16_grad<3, G::BT, G::CAP, G::W><<<(unsigned)((a.n + G::BT - 1) / G::BT), G::BT, 0, st>>>(a);
+    launch_pdl(k_r16_grad<3, G::BT, G::CAP, G::W>, (unsigned)((a.n + G::BT - 1) / G::BT), G::BT,
+               st, a);
     return 1;
   }
   return 0;
@@ -1648,6 +1677,8 @@ constexpr size_t enc_smem_bytes() {
 
 template <int D, int P, int MODE>
 __global__ void __launch_bounds__(EncShape<D, P>::BT) k_encode_rows(EncArgs e, SweepArgs a) {
+  // (no programmatic-launch trigger: the 2-D sweep launched early behind this
+  // grid measured 149 vs 137 us at C2; the 3-D chain gains 615 -> 610 us)
   using E = EncShape<D, P>;
   using L = ChunkLay<D, P, MODE>;
   using T = typename Prec<P>::T;
@@ -1945,6 +1976,7 @@ constexpr size_t xy_smem_bytes() {
 }
 
 __global__ void __launch_bounds__(XYShape::BT) k_encode_xy(EncArgs e, SweepArgs a) {
+  pdl_trigger();  // the tests may launch once every encode CTA has started
   using S = XYShape;
   using L = ChunkLay<3, FP16, MODE_RCLL>;
   constexpr int XB = S::XB, BT = S::BT, NW = S::NW, NWC = 3 * NW;
@@ -2315,15 +2347,15 @@ static int64_t sweep_t(const SweepArgs& a, cudaStream_t st) {
   if constexpr (P == FP16 && M == MODE_RCLL && D == 3) {
     // 3-D: tests and ordered emission in separate kernels (R16Two)
     using R = R16Two<D>;
-    k_r16_test<D><<<(unsigned)((a.n + R::TB - 1) / R::TB), R::TB, 0, st>>>(a);
+    launch_pdl(k_r16_test<D>, (unsigned)((a.n + R::TB - 1) / R::TB), R::TB, st, a);
     if (a.nrows > R::LARGE_ROWS) {
       const int64_t nb = (a.nrows + R::BT_LARGE - 1) / R::BT_LARGE;
-      k_r16_emit<D, R::BT_LARGE, R::BT_LARGE * R::PCAP_ROW>
-          <<<(unsigned)nb, R::BT_LARGE, 0, st>>>(a);
+      launch_pdl(k_r16_emit<D, R::BT_LARGE, R::BT_LARGE * R::PCAP_ROW>, (unsigned)nb,
+                 R::BT_LARGE, st, a);
       return nb;
     }
     const int64_t nb = (a.nrows + R::BT - 1) / R::BT;
-    k_r16_emit<D, R::BT, R::BT * R::PCAP_ROW><<<(unsigned)nb, R::BT, 0, st>>>(a);
+    launch_pdl(k_r16_emit<D, R::BT, R::BT * R::PCAP_ROW>, (unsigned)nb, R::BT, st, a);
     return nb;
   } else if constexpr (P == FP16 && M == MODE_RCLL && D == 2) {
     // 2-D: one fused kernel (the look-back wait hides the emission)
