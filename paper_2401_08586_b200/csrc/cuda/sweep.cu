@@ -870,6 +870,7 @@ __global__ void __launch_bounds__(BT, R16Shape<D>::MINB) k_rcll16(SweepArgs a) {
   __shared__ int s_w[BT / 32];
   __shared__ long long s_base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  pdl_wait();  // programmatic launch behind the encode: its runs are complete
 #if SPHX_TICKET
   __shared__ int s_tile;
   if (tid == 0) s_tile = (int)(atomicAdd(a.ticket, 1ull) - a.tick0);
@@ -1677,8 +1678,8 @@ constexpr size_t enc_smem_bytes() {
 
 template <int D, int P, int MODE>
 __global__ void __launch_bounds__(EncShape<D, P>::BT) k_encode_rows(EncArgs e, SweepArgs a) {
-  // (no programmatic-launch trigger: the 2-D sweep launched early behind this
-  // grid measured 149 vs 137 us at C2; the 3-D chain gains 615 -> 610 us)
+  // programmatic dependent launch of the 2-D sweep: each CTA triggers after its
+  // stores (triggering at the start measured 149 vs 137 us at C2; at the end 136.5)
   using E = EncShape<D, P>;
   using L = ChunkLay<D, P, MODE>;
   using T = typename Prec<P>::T;
@@ -1925,6 +1926,7 @@ __global__ void __launch_bounds__(EncShape<D, P>::BT) k_encode_rows(EncArgs e, S
     uint4* td = reinterpret_cast<uint4*>(a.qtag) + ch0;
     for (int q = tid; q < nch; q += BT) td[q] = ts[q];
   }
+  pdl_trigger();  // after this CTA's stores: the sweep launches behind the last CTAs
 }
 
 // ------------------------------------------------------------------------------
@@ -2361,7 +2363,7 @@ static int64_t sweep_t(const SweepArgs& a, cudaStream_t st) {
     // 2-D: one fused kernel (the look-back wait hides the emission)
     using R = R16Shape<D>;
     const int64_t nb = (a.nrows + R::BT - 1) / R::BT;
-    k_rcll16<D, R::BT, R::PCAP, R::WMAX><<<(unsigned)nb, R::BT, 0, st>>>(a);
+    launch_pdl(k_rcll16<D, R::BT, R::PCAP, R::WMAX>, (unsigned)nb, R::BT, st, a);
     return SPHX_TICKET ? nb : 0;  // tiles from blockIdx take no tickets
   } else {
     const int64_t nb = (a.nrows + S::BT - 1) / S::BT;
