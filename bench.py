@@ -42,8 +42,15 @@ WORKLOADS = {
                desc="C4 3-D dam-break column 200x400x200 (16M particles) in the unit cube, "
                     "FP16 RCLL"),
     # un-jittered 640^3 lattice, generated on the device
+    # per GPU under weak scaling: 640 x 640 x 80 (32.8M), stacked along z
     "C5": dict(dim=3, ds=1.0 / 640, jitter=0.0, seed=1, device_lattice=True,
+               weak_sites=(640, 640, 80),
                desc="C5 3-D lattice 640^3 (262M particles), FP16 RCLL"),
+    # C5's construction at 96^3 (884K; 96 x 96 x 24 per GPU under weak scaling): the
+    # multi-rank checks in tests/test_multigpu.py
+    "C5s": dict(dim=3, ds=1.0 / 96, jitter=0.0, seed=1, device_lattice=True,
+                weak_sites=(96, 96, 24),
+                desc="C5s 3-D lattice 96^3 (C5's construction, test size), FP16 RCLL"),
 }
 PREC = {"fp64": 0, "fp32": 1, "fp16": 2}
 
@@ -67,7 +74,34 @@ def parse():
                          "lattice order, a seeded random shuffle, or cell-major order")
     ap.add_argument("--slab", action="store_true",
                     help="use the slab-decomposed (multi-GPU) path even at N=1")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak stacks the per-GPU lattice N times along the slab axis "
+                         "(C5: 640x640x80 per GPU), strong splits the whole config N ways")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="N ranks on cuda:0 with a host-staged gloo halo exchange (proves the "
+                         "N > 1 path on a one-GPU lease; NCCL needs one GPU per rank)")
     return ap.parse_args()
+
+
+def relaunch(args):
+    """`bench.py --gpus N` (N > 1) outside torchrun: run N ranks of this script
+    (one process per GPU) and pass rank 0's line through."""
+    import socket
+    import subprocess
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            sys.exit(f"--gpus {args.gpus} under a launcher with WORLD_SIZE={world}")
+        return
+    if args.gpus <= 1:
+        return
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.run(cmd).returncode)
 
 
 def measured_peaks():
@@ -194,7 +228,7 @@ def run_reference(args):
         step()
     ts = [step() for _ in range(args.steps)]
     # ref_time_nnps(…, repeats=1) = one discarded warm-up + one timed call per step
-    t = statistics.mean(ts)
+    t = statistics.median(ts)
     v = n / t
     line = {"metric": METRIC, "value": v, "unit": "particles/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
@@ -369,7 +403,7 @@ def run_ours(args):
     if world > 1 or args.slab:
         from paper_2401_08586_b200 import multigpu
         return multigpu.bench(args, WORKLOADS, METRIC, clock_sampler=ClockSampler,
-                              peaks=measured_peaks(), golden=golden)
+                              peaks=measured_peaks())
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -512,9 +546,9 @@ def run_ours(args):
         parity = sampled_parity(args.config, w, grid, prec, rel, cell, start, items, offsets, out,
                                 total)
 
-    t_step = statistics.mean(step_ms) * 1e-3
-    t_sweep = statistics.mean(sweep_ms) * 1e-3
-    t_e2e = statistics.mean(e2e_t) if e2e_t else None
+    t_step = statistics.median(step_ms) * 1e-3
+    t_sweep = statistics.median(sweep_ms) * 1e-3
+    t_e2e = statistics.median(e2e_t) if e2e_t else None
     s_pos = {0: 8, 1: 4, 2: 2}[prec] * dim
     b_sweep = n * s_pos + 4 * n + 4 * (C + 1) + 8 * (n + 1) + 4 * total
     b_pipe = b_sweep + 8 * dim * n + 4 * dim * n + 4 * n + n * (s_pos + 4)
@@ -536,7 +570,7 @@ def run_ours(args):
                    "order": args.order,
                    "l2": "flushed between timed steps (256 MiB write, outside the events)"},
         "parity": parity,
-        "breakdown_ms": {"encode": statistics.mean(encode_ms), "sweep": t_sweep * 1e3,
+        "breakdown_ms": {"encode": statistics.median(encode_ms), "sweep": t_sweep * 1e3,
                          "step": t_step * 1e3, "wall_per_step": t_wall / args.steps * 1e3},
         "roofline": {"bound": "hbm",
                      "kernel": ("k_rcll16 (single pass: tests, sorted rows, tile look-back, "
@@ -605,7 +639,7 @@ def bench_grad(args, w, ctx, stream, grid, n, C, xd, rel, cell, items, start, lo
             step()
             ev[k][1].record(stream)
         torch.cuda.synchronize()
-    t = statistics.mean(a.elapsed_time(b) for a, b in ev) * 1e-3
+    t = statistics.median(a.elapsed_time(b) for a, b in ev) * 1e-3
     # parity: the oracle's grad_normalized on the oracle's FP16 RCLL table
     orc = O.Oracle()
     xh = [a.cpu().numpy() for a in xd]
@@ -723,7 +757,7 @@ def bench_step(args, w, ctx, stream, grid, n, C, xd, rel, cell, cell_of, items, 
             step()
             ev[k][1].record(stream)
         torch.cuda.synchronize()
-    t = statistics.mean(a.elapsed_time(b) for a, b in ev) * 1e-3
+    t = statistics.median(a.elapsed_time(b) for a, b in ev) * 1e-3
     total = int(off[n].item())
     # algorithmic bytes: the NNPS step's + the FP64 state (x, v, m, rho, p, e read,
     # x, v, rho, p, e, rel written) + the table read twice (stress, rates)
@@ -761,6 +795,7 @@ def main():
     if os.environ.get("NCCL_DEBUG", "").upper() in ("VERSION", "WARN"):
         del os.environ["NCCL_DEBUG"]
     args = parse()
+    relaunch(args)
     if args.impl == "reference":
         run_reference(args)
     else:

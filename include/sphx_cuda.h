@@ -196,6 +196,23 @@ int sphx_build_rel_coords_window_device(sphx_context* ctx, const sphx_grid_desc*
                                         int32_t* d_cell_of, int32_t* d_cell_start,
                                         int32_t* d_items);
 
+/* Multi-GPU slab assembly after a halo exchange (no binning). A rank holds its
+ * owned particles in CSR order in slots [0, n_own) with d_owned_start = the CSR
+ * start over its owned layers (nl * CL + 1 entries, from 0; CL = cells per
+ * layer of the slab axis, the slowest axis of linear_cell, cell_grid.hpp:74-78).
+ * The neighbours' boundary layers arrive as contiguous RelCoords / id slices in
+ * slots [slot_below, ...) and [slot_above, ...) together with their slices of
+ * cell_start (CL + 1 entries, any base; NULL = a wall, no halo). Writes the
+ * local CellGrid of local->counts[axis] = nl + 2 layers (lower halo, owned, upper
+ * halo): d_cell_start, d_items (CSR position -> slot) and RelCoords::cell of the
+ * halo slots (their cell; the slab-axis coordinate 0 or nl + 1). Sizes are read
+ * on the device: stream-ordered, no synchronisation. */
+int sphx_slab_assemble_device(sphx_context* ctx, const sphx_grid_desc* local, int32_t axis,
+                              int64_t n_own, int64_t slot_below, int64_t slot_above,
+                              int64_t n_slots, const int32_t* d_owned_start,
+                              const int32_t* d_recv_below, const int32_t* d_recv_above,
+                              int32_t* d_cell_start, int32_t* d_items, int32_t* const d_cell[3]);
+
 /* RCLL rows for particles [row0, row0 + nrows) only (the owned particles of a
  * slab); neighbour ids are written as d_ids[j] (global ids; NULL = local j).
  * d_offsets has nrows + 1 entries; d_offsets[nrows] = exact total. */

@@ -92,6 +92,8 @@ def lib():
                                             vp, i64]),
         "sphx_lattice_device": (C.c_int, [vp, i32, C.POINTER(dbl), C.POINTER(dbl), dbl, i64, i64,
                                           p3]),
+        "sphx_slab_assemble_device": (C.c_int, [vp, G, i32, i64, i64, i64, i64, vp, vp, vp, vp,
+                                                vp, p3]),
         "sphx_rcll_distances_device": (C.c_int, [vp, G, i64, p3, p3, i32, vp, vp, vp]),
         "sphx_table_distances": (C.c_int, [vp, G, i32, vp]),
         "sphx_update_relative": (C.c_int, [vp, G, i64, p3, p3, p3, i32]),
@@ -125,7 +127,7 @@ EXPORTED = ("sphx_last_error", "sphx_grid_init", "sphx_create", "sphx_destroy",
             "sphx_lattice_device", "sphx_rcll_distances_device", "sphx_table_distances",
             "sphx_rcll_grad_normalized", "sphx_rcll_grad_normalized_device",
             "sphx_update_relative", "sphx_update_relative_device", "sphx_rebuild_members_device",
-            "sphx_step_mixed_device", "sphx_build_gapped_random")
+            "sphx_step_mixed_device", "sphx_build_gapped_random", "sphx_slab_assemble_device")
 
 APPROACH_I, APPROACH_II, APPROACH_III = 0, 1, 2
 
@@ -490,6 +492,16 @@ class Context:
             self.h, C.byref(grid), rel[0].numel(), _dptr3(rel), _dptr3(cell), items.data_ptr(),
             cell_start.data_ptr(), prec, ids.data_ptr() if ids is not None else None, row0, nrows,
             offsets.data_ptr(), items_out.data_ptr(), items_out.numel()))
+
+    def slab_assemble_device(self, local_grid, axis, n_own, slot_below, slot_above, n_slots,
+                             owned_start, recv_below, recv_above, cell_start, items, cell):
+        """Local CellGrid of a slab after its halo exchange (sphx_slab_assemble_device)."""
+        self._bind(cell_start)
+        ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+        check(lib().sphx_slab_assemble_device(
+            self.h, C.byref(local_grid), axis, n_own, slot_below, slot_above, n_slots,
+            owned_start.data_ptr(), ptr(recv_below), ptr(recv_above), cell_start.data_ptr(),
+            items.data_ptr(), _dptr3(cell)))
 
     def lattice_device(self, dim, lo, hi, ds, id0, x):
         self._bind(x[0])

@@ -80,8 +80,11 @@ __global__ void k_locate(LocateArgs a) {
       double r;
       locate_axis(g, k, xn, c[k], r);
       if (k == g.win_axis) {  // global layer -> slab-local layer (periodic wrap)
-        c[k] = (c[k] - g.win_lo + g.win_global) % g.win_global;
-        if (c[k] >= g.counts[k]) c[k] = g.counts[k] - 1;  // outside the window: malformed
+        int d = c[k] - g.win_lo;
+        if (d < 0) d += g.win_global;
+        else if (d >= g.counts[k]) d -= g.win_global;  // a window longer than the axis
+        if (d < 0 || d >= g.counts[k]) d = g.counts[k] - 1;  // outside the window: malformed
+        c[k] = d;
       }
       if (MODE == BIN_REL) {
         a.rel_out[k][i] = r;

@@ -52,6 +52,8 @@ int launch_kick_drift(int dim, const StepArgs& a, cudaStream_t st);
 void tiled2_shape(int nx, int ny, int64_t n, int* tw, int* tpr, int64_t* ntiles);
 int64_t tiled2_scan_tiles(int64_t nrows);
 int launch_tiled2(const TileArgs& a, bool count, cudaStream_t st);
+// slab.cu
+int launch_slab_assemble(const SlabArgs& a, cudaStream_t st);
 }  // namespace sphx_dev
 
 using namespace sphx_dev;
@@ -1234,6 +1236,47 @@ int sphx_rcll_rows_device(sphx_context* ctx, const sphx_grid_desc* grid, int64_t
   TRY(run_prepare(ctx, MODE_RCLL, *grid, n, d_rel, d_cell, d_items, d_cell_start, nullptr,
                   precision, 0.0, d_offsets, &a, sel));
   return run_sweep(ctx, grid->dim, precision, MODE_RCLL, a, d_items_out, capacity);
+}
+
+int sphx_slab_assemble_device(sphx_context* ctx, const sphx_grid_desc* local, int32_t axis,
+                              int64_t n_own, int64_t slot_below, int64_t slot_above,
+                              int64_t n_slots, const int32_t* d_owned_start,
+                              const int32_t* d_recv_below, const int32_t* d_recv_above,
+                              int32_t* d_cell_start, int32_t* d_items, int32_t* const d_cell[3]) {
+  TRY(check_ctx(ctx));
+  if (!local || !d_owned_start || !d_cell_start || !d_items || !d_cell)
+    return fail(SPHX_ERR_INVALID_ARGUMENT, "null argument");
+  TRY(check_prec_dim(SPHX_FP64, local->dim));
+  if (axis < 0 || axis >= local->dim || local->counts[axis] < 3)
+    return fail(SPHX_ERR_INVALID_ARGUMENT, "bad slab axis");
+  if (n_own < 0 || slot_below < n_own || slot_above < slot_below || n_slots < slot_above ||
+      n_slots > INT32_MAX)
+    return fail(SPHX_ERR_INVALID_ARGUMENT, "bad slab slots");
+  SlabArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.dim = local->dim;
+  a.axis = axis;
+  a.CL = 1;
+  for (int k = 0; k < local->dim; ++k) {
+    a.cnt[k] = local->counts[k];
+    if (k != axis) a.CL *= local->counts[k];
+  }
+  a.nl = local->counts[axis] - 2;
+  a.n_own = (int)n_own;
+  a.slotB = (int)slot_below;
+  a.slotA = (int)slot_above;
+  a.n_slots = (int)n_slots;
+  a.haveB = d_recv_below != nullptr;
+  a.haveA = d_recv_above != nullptr;
+  a.ocs = d_owned_start;
+  a.rB = d_recv_below;
+  a.rA = d_recv_above;
+  a.start = d_cell_start;
+  a.items = d_items;
+  for (int k = 0; k < 3; ++k) a.cell[k] = k < local->dim ? d_cell[k] : nullptr;
+  ctx->launches += launch_slab_assemble(a, ctx->stream);
+  CKL();
+  return SPHX_OK;
 }
 
 int sphx_build_rel_coords_window_device(sphx_context* ctx, const sphx_grid_desc* global,

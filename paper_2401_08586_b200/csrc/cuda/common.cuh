@@ -100,6 +100,21 @@ struct TileArgs {
   unsigned epoch;
 };
 
+// Slab assembly after a halo exchange (slab.cu)
+struct SlabArgs {
+  int dim, axis, CL, nl;       // CL = cells per layer; nl = owned layers
+  int cnt[3];                  // local grid counts (axis: nl + 2)
+  int n_own, slotB, slotA;     // first slot of the lower / upper halo
+  int haveB, haveA;            // 0: a wall, no halo on that side
+  const int32_t* ocs;          // owned CSR start over layers 1..nl [nl*CL + 1], from 0
+  const int32_t* rB;           // received cell_start slice of the lower halo [CL + 1]
+  const int32_t* rA;           // ... of the upper halo
+  int32_t* start;              // local cell_start [(nl + 2) * CL + 1]
+  int32_t* items;              // local CSR -> slot [n_slots]
+  int32_t* cell[3];            // RelCoords::cell of the halo slots (written)
+  int n_slots;
+};
+
 // Look-back words carry flag and value in one 64-bit word, so relaxed gpu-scope
 // accesses suffice. (An acquire load would compile to CCTL.IVALL -- an L1
 // invalidation per spin iteration that evicts every warp's cached candidates.)

@@ -7,21 +7,28 @@ the global neighbour table is partitioned by owner:
 * The global CellGrid's slowest axis (y in 2-D, z in 3-D, x in 1-D) is cut into
   ``world`` contiguous ranges of whole cell layers (``SlabPlan``). Rank r owns
   the particles whose cell lies in its layers.
-* Each rank receives one halo layer from each neighbour (rank +- 1, wrapping when
-  the axis is periodic with > 2 layers, the reference's wrap rule nnps.cpp:223)
-  over ``torch.distributed`` point-to-point (NCCL on GPUs, gloo in the CPU tests).
-* The rank bins owned + halo particles on the GLOBAL grid
-  (``sphx_build_rel_coords_window_device``: global normalisation, cell choice
-  and Eq. 6 rel bit-identical to the one-GPU run) into a local grid of
-  ``nl + 2`` layers with the axis non-periodic, then produces the rows of its
-  owned particles only (``sphx_rcll_rows_device``) with global ids as neighbour
-  ids. Local arrays are [owned | halo below | halo above], each part in
-  ascending global id, so every candidate run is in global-id order and the
-  rows come out exactly as the reference's (sorted ascending, nnps.cpp:54).
+* Each rank keeps its owned particles' RelCoords (on the GLOBAL grid: global
+  normalisation, cell choice and Eq. 6 rel bit-identical to one GPU) resident in
+  CSR order. The linear cell index is x-fastest (cell_grid.hpp:74-78), so a cell
+  layer is a contiguous range of CSR positions: the first and the last owned
+  layer are a prefix and a suffix of the rank's arrays.
+* A call exchanges those two layers with the neighbouring ranks (rank +- 1,
+  wrapping when the axis is periodic with > 2 layers, the reference's wrap rule
+  nnps.cpp:223): the rel slice of each axis (FP64, the drop-in's RelCoords), the
+  global ids and the layer's slice of cell_start. Messages have a fixed capacity
+  agreed once (the largest boundary layer), so no size round trip and no host
+  synchronisation: NCCL point-to-point on GPUs (``exchange_nccl``), host-staged
+  gloo when several ranks share one GPU (``exchange_gloo``).
+* ``sphx_slab_assemble_device`` writes the local CellGrid of nl + 2 layers
+  (lower halo, owned, upper halo) from device-side sizes, and
+  ``sphx_rcll_rows_device`` produces the rows of the owned particles with global
+  ids as neighbour ids. The rows come out sorted exactly as the reference's
+  (nnps.cpp:54): every cell's members are ascending in global id.
 
 The union of the per-rank tables, rows placed by global id, is the one-GPU
-table bit for bit (tests/test_multigpu.py checks it on one GPU with two slabs,
-and the partition + exchange logic on CPU with gloo, world_size 2).
+table bit for bit (tests/test_multigpu.py: several slabs on one GPU, and ranks
+over gloo sharing a GPU); the exchange protocol is also checked on CPU (gloo,
+world_size 2 and 3).
 """
 from __future__ import annotations
 
@@ -71,34 +78,26 @@ class SlabPlan:
         return hi - lo
 
     def prev(self, r: int):
-        """Rank holding the layer just below rank r's slab (None at a wall)."""
-        if self.world == 1:
-            return None
+        """Rank holding the layer just below rank r's slab (None at a wall; r itself
+        for one rank on a periodic axis)."""
         if r > 0:
             return r - 1
         return self.world - 1 if self.wrap else None
 
     def next(self, r: int):
-        if self.world == 1:
-            return None
         if r < self.world - 1:
             return r + 1
         return 0 if self.wrap else None
 
     def layer0(self, r: int) -> int:
         """Global layer of local layer 0 (the lower halo; -1 = below a wall)."""
-        return self.bounds[r][0] - 1 if self.world > 1 else 0
-
-    def local_layer_counts(self, r: int) -> int:
-        return self.nlayers(r) + 2 if self.world > 1 else self.G
+        return self.bounds[r][0] - 1
 
     def local_grid(self, grid, r: int):
         """The rank's CellGrid descriptor: the global one with nl + 2 layers along
         the slab axis, not periodic there (the halos carry the wrap)."""
-        if self.world == 1:
-            return grid
         g = type(grid).from_buffer_copy(grid)
-        g.counts[self.axis] = self.local_layer_counts(r)
+        g.counts[self.axis] = self.nlayers(r) + 2
         g.periodic[self.axis] = 0
         return g
 
@@ -108,163 +107,122 @@ class SlabPlan:
         return np.searchsorted(edges, np.asarray(layer), side="right")
 
 
+def cells_per_layer(grid, axis: int) -> int:
+    return int(np.prod([grid.counts[k] for k in range(grid.dim) if k != axis]))
+
+
 # ---------------------------------------------------------------------------------------
-# halo exchange (the only collective on the path)
+# one rank's slab
 # ---------------------------------------------------------------------------------------
-def pack(x, ids, sel) -> torch.Tensor:
-    """[dim + 1, m] float64 message: positions, then global ids (exact in fp64)."""
-    rows = [a[sel] for a in x] + [ids[sel].to(torch.float64)]
-    return torch.stack(rows) if rows[0].numel() else torch.empty(
-        (len(rows), 0), dtype=torch.float64, device=ids.device)
+class SlabState:
+    """A rank's resident slab: owned RelCoords in CSR order + reserved halo slots.
 
-
-def unpack(buf: torch.Tensor, dim: int):
-    x = [buf[k].contiguous() for k in range(dim)]
-    ids = buf[dim].to(torch.int32)
-    return x, ids
-
-
-def exchange_halo(plan: SlabPlan, rank: int, send_down: torch.Tensor, send_up: torch.Tensor,
-                  group=None):
-    """Send the first owned layer to prev (its upper halo) and the last owned layer
-    to next (its lower halo); returns (halo_below, halo_above) messages.
-
-    Operations are posted in the same order on every rank, so the in-order
-    matching of NCCL point-to-point pairs them correctly even when prev == next
-    (world 2, periodic); gloo matches on the tags.
+    Slots: [owned (n_own) | pad (cap) | lower halo (cap) | upper halo (cap)]. The pad
+    lets the last-layer message be a fixed-size slice starting inside the owned part.
     """
-    prv, nxt = plan.prev(rank), plan.next(rank)
-    dev = send_down.device
-    rows = send_down.shape[0]
-
-    def ops_for(down, up, from_next, from_prev):
-        ops = []
-        if prv is not None:
-            ops.append(dist.P2POp(dist.isend, down, prv, group=group, tag=0))
-        if nxt is not None:
-            ops.append(dist.P2POp(dist.isend, up, nxt, group=group, tag=1))
-        if nxt is not None:
-            ops.append(dist.P2POp(dist.irecv, from_next, nxt, group=group, tag=0))
-        if prv is not None:
-            ops.append(dist.P2POp(dist.irecv, from_prev, prv, group=group, tag=1))
-        return ops
-
-    def run(ops):
-        if ops:
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
-
-    # sizes, then payloads (at least one column so no zero-byte messages)
-    sz_down = torch.tensor([send_down.shape[1]], dtype=torch.int64, device=dev)
-    sz_up = torch.tensor([send_up.shape[1]], dtype=torch.int64, device=dev)
-    sz_next = torch.zeros(1, dtype=torch.int64, device=dev)
-    sz_prev = torch.zeros(1, dtype=torch.int64, device=dev)
-    run(ops_for(sz_down, sz_up, sz_next, sz_prev))
-    m_next, m_prev = int(sz_next.item()), int(sz_prev.item())
-
-    def padded(buf):
-        if buf.shape[1] > 0:
-            return buf.contiguous()
-        return torch.zeros((rows, 1), dtype=torch.float64, device=dev)
-
-    r_next = torch.empty((rows, max(m_next, 1)), dtype=torch.float64, device=dev)
-    r_prev = torch.empty((rows, max(m_prev, 1)), dtype=torch.float64, device=dev)
-    run(ops_for(padded(send_down), padded(send_up), r_next, r_prev))
-    return r_prev[:, :m_prev], r_next[:, :m_next]
-
-
-def exchange_local(plan: SlabPlan, downs, ups):
-    """The same exchange between slabs held by one process (single-GPU tests)."""
-    out = []
-    for r in range(plan.world):
-        prv, nxt = plan.prev(r), plan.next(r)
-        below = ups[prv] if prv is not None else downs[r][:, :0]
-        above = downs[nxt] if nxt is not None else downs[r][:, :0]
-        out.append((below, above))
-    return out
-
-
-# ---------------------------------------------------------------------------------------
-# one rank's slab on its GPU
-# ---------------------------------------------------------------------------------------
-class Slab:
-    """Owned particles (ascending global ids) + halos, binned and swept on one GPU."""
 
     def __init__(self, ctx: capi.Context, grid, plan: SlabPlan, rank: int, x_owned, ids_owned):
+        if plan.world == 1 and plan.wrap:
+            raise ValueError("one slab on a periodic axis: use the one-GPU path")
         self.ctx, self.grid, self.plan, self.rank = ctx, grid, plan, rank
-        self.local = plan.local_grid(grid, rank)
         self.dim = grid.dim
-        self.x_owned = [a.contiguous() for a in x_owned]
-        self.ids_owned = ids_owned.contiguous()
-        self.n_owned = int(ids_owned.numel())
+        self.axis = plan.axis
+        self.local = plan.local_grid(grid, rank)
+        self.CL = cells_per_layer(grid, self.axis)
+        self.nl = plan.nlayers(rank)
         self.device = ids_owned.device
-        self.layer = None  # local slab-axis layer of each owned particle (after bin())
-        self.n = 0
-
-    # -- halo ---------------------------------------------------------------------------
-    def boundary(self, layer_global=None):
-        """(first-layer message, last-layer message) of the owned particles."""
-        if self.plan.world == 1:
-            e = torch.empty((self.dim + 1, 0), dtype=torch.float64, device=self.device)
-            return e, e
-        if layer_global is not None:
-            L0, L1 = self.plan.owned(self.rank)
-            first, last = layer_global == L0, layer_global == L1 - 1
-        else:
-            first, last = self.layer == 1, self.layer == self.plan.nlayers(self.rank)
-        return pack(self.x_owned, self.ids_owned, first), pack(self.x_owned, self.ids_owned, last)
-
-    def assemble(self, below: torch.Tensor, above: torch.Tensor):
-        """Local arrays [owned | halo below | halo above] (each ascending in id)."""
-        xb, ib = unpack(below, self.dim)
-        xa, ia = unpack(above, self.dim)
-        self.x = [torch.cat([o, b, a]).contiguous()
-                  for o, b, a in zip(self.x_owned, xb, xa)]
-        self.ids = torch.cat([self.ids_owned, ib, ia]).contiguous()
-        self.n = int(self.ids.numel())
-        self._alloc()
-
-    def _alloc(self):
-        """Grow-only device buffers (re-used across refresh() calls)."""
         dev = self.device
-        if getattr(self, "_cap", -1) < self.n:
-            self._cap = n = max(self.n + self.n // 8, 1)
-            self.rel = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(self.dim)]
-            self.cell = [torch.empty(n, dtype=torch.int32, device=dev) for _ in range(self.dim)]
-            self.cell_of = torch.empty(n, dtype=torch.int32, device=dev)
-            self.items = torch.empty(n, dtype=torch.int32, device=dev)
-        if not hasattr(self, "start"):
-            self.start = torch.empty(self.local.cell_total + 1, dtype=torch.int32, device=dev)
-            self.offsets = torch.empty(self.n_owned + 1, dtype=torch.int64, device=dev)
-            per = {1: 8, 2: 24, 3: 80}[self.dim]
-            self.out = torch.empty(max(self.n_owned * per, 1), dtype=torch.int32, device=dev)
-
-    def _view(self, ts):
-        return [t[: self.n] for t in ts]
-
-    # -- binning + rows -----------------------------------------------------------------
-    def bin(self):
-        """Window binning of the local particles on the global grid."""
-        x, rel, cell = self._view(self.x), self._view(self.rel), self._view(self.cell)
-        if self.plan.world == 1:
-            self.ctx.build_rel_coords_device(self.grid, x, rel, cell, self.cell_of[: self.n],
-                                             self.start, self.items[: self.n])
+        n = int(ids_owned.numel())
+        self.n_own = n
+        # owned particles on the global grid, binned into the local window (layers 1..nl)
+        rel = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(self.dim)]
+        cell = [torch.empty(n, dtype=torch.int32, device=dev) for _ in range(self.dim)]
+        cell_of = torch.empty(n, dtype=torch.int32, device=dev)
+        start = torch.empty(self.local.cell_total + 1, dtype=torch.int32, device=dev)
+        items = torch.empty(n, dtype=torch.int32, device=dev)
+        if n:
+            ctx.build_rel_coords_window_device(grid, self.local, self.axis, plan.layer0(rank),
+                                               [a.contiguous() for a in x_owned], rel, cell,
+                                               cell_of, start, items)
         else:
-            self.ctx.build_rel_coords_window_device(
-                self.grid, self.local, self.plan.axis, self.plan.layer0(self.rank), x, rel, cell,
-                self.cell_of[: self.n], self.start, self.items[: self.n])
-        self.layer = self.cell[self.plan.axis][: self.n_owned]
+            start.zero_()
+        perm = items.long()  # CSR order: the boundary layers become a prefix and a suffix
+        self._rel_o = [r[perm] for r in rel]
+        self._cell_o = [c[perm] for c in cell]
+        self._ids_o = ids_owned[perm].contiguous()
+        CL, nl = self.CL, self.nl
+        st = start.cpu().numpy().astype(np.int64)
+        if st[CL] != 0 or st[(nl + 1) * CL] != n:
+            raise RuntimeError("owned particles outside the rank's layers")
+        self.owned_start = start[CL: (nl + 1) * CL + 1].contiguous()
+        self.first_count = int(st[2 * CL] - st[CL])           # layer 1
+        self.last_begin = int(st[nl * CL] - st[CL])            # layer nl
+        self.last_count = n - self.last_begin
+        self.cap = None
+
+    def boundary_max(self) -> int:
+        return max(self.first_count, self.last_count, 1)
+
+    def allocate(self, cap: int):
+        """Slot arrays for a fixed message capacity (the largest boundary layer)."""
+        dev, n, d = self.device, self.n_own, self.dim
+        self.cap = int(cap)
+        self.slot_below = n + self.cap
+        self.slot_above = n + 2 * self.cap
+        self.n_slots = n + 3 * self.cap
+        self.rel = [torch.zeros(self.n_slots, dtype=torch.float64, device=dev) for _ in range(d)]
+        self.cell = [torch.zeros(self.n_slots, dtype=torch.int32, device=dev) for _ in range(d)]
+        self.ids = torch.zeros(self.n_slots, dtype=torch.int32, device=dev)
+        for k in range(d):
+            self.rel[k][:n] = self._rel_o[k]
+            self.cell[k][:n] = self._cell_o[k]
+        self.ids[:n] = self._ids_o
+        del self._rel_o, self._cell_o, self._ids_o
+        self.recv_start = [torch.zeros(self.CL + 1, dtype=torch.int32, device=dev)
+                           for _ in range(2)]
+        self.start = torch.empty(self.local.cell_total + 1, dtype=torch.int32, device=dev)
+        self.items = torch.empty(self.n_slots, dtype=torch.int32, device=dev)
+        self.offsets = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        per = {1: 8, 2: 24, 3: 64}[self.dim]
+        self.out = torch.empty(max(n * per, 1), dtype=torch.int32, device=dev)
+
+    # -- messages -------------------------------------------------------------------------
+    def send(self, side: int):
+        """Side 0: the first owned layer (to prev); side 1: the last (to next). Fixed
+        sizes: rel[k] (cap), ids (cap), cell_start slice (CL + 1)."""
+        b = 0 if side == 0 else self.last_begin
+        s0 = 0 if side == 0 else (self.nl - 1) * self.CL
+        return ([r[b: b + self.cap] for r in self.rel] + [self.ids[b: b + self.cap]]
+                + [self.owned_start[s0: s0 + self.CL + 1]])
+
+    def recv(self, side: int):
+        """Side 0: the lower halo (from prev); side 1: the upper halo (from next)."""
+        b = self.slot_below if side == 0 else self.slot_above
+        return ([r[b: b + self.cap] for r in self.rel] + [self.ids[b: b + self.cap]]
+                + [self.recv_start[side]])
+
+    def has(self, side: int) -> bool:
+        return (self.plan.prev(self.rank) if side == 0 else self.plan.next(self.rank)) is not None
+
+    # -- per call ------------------------------------------------------------------------
+    def assemble(self):
+        self.ctx.slab_assemble_device(
+            self.local, self.axis, self.n_own, self.slot_below, self.slot_above, self.n_slots,
+            self.owned_start, self.recv_start[0] if self.has(0) else None,
+            self.recv_start[1] if self.has(1) else None, self.start, self.items, self.cell)
 
     def rows(self, prec: int):
-        """Rows of the owned particles into self.offsets / self.out (device API:
-        no synchronisation; returns nothing)."""
-        self.ctx.rcll_rows_device(self.local, self._view(self.rel), self._view(self.cell),
-                                  self.items[: self.n], self.start, prec, self.ids[: self.n], 0,
-                                  self.n_owned, self.offsets, self.out)
+        self.ctx.rcll_rows_device(self.local, self.rel, self.cell, self.items, self.start, prec,
+                                  self.ids, 0, self.n_own, self.offsets, self.out)
 
-    def rows_sized(self, prec: int) -> int:
-        """rows() growing the output to the exact total (one host sync)."""
+    def step(self, prec: int, exchange):
+        """One NNPS call of the rank: halo exchange -> local CellGrid -> owned rows."""
+        exchange(self)
+        self.assemble()
         self.rows(prec)
+
+    def size_output(self, prec: int) -> int:
+        """Grow the row buffer to the exact total (one host sync, setup only)."""
         total = int(self.offsets[-1].item())
         if total > self.out.numel():
             self.out = torch.empty(total + total // 16 + 1024, dtype=torch.int32,
@@ -272,49 +230,142 @@ class Slab:
             self.rows(prec)
         return total
 
-    def refresh(self, prec: int, exchange):
-        """Full per-call pipeline: halo exchange -> window binning -> rows."""
-        down, up = self.boundary()
-        below, above = exchange(down, up)
-        self.assemble(below, above)
-        self.bin()
-        self.rows(prec)
+
+# ---------------------------------------------------------------------------------------
+# halo exchange (the only collective on the path)
+# ---------------------------------------------------------------------------------------
+def _coll_device(device):
+    """Collectives run on the device under NCCL, on the host under gloo."""
+    return device if dist.get_backend() == "nccl" else torch.device("cpu")
 
 
-def owned_from_global(ctx: capi.Context, grid, plan: SlabPlan, rank: int, x_host, device,
-                      chunk: int = 1 << 22):
-    """Owned particles of `rank` out of a host-resident global system: locate every
-    particle on the device (global grid), keep those in the rank's layers.
-    Returns (x list, global ids, global layer), ascending in id."""
+def agree_capacity(state: SlabState, group=None) -> int:
+    """Largest boundary layer over all ranks (once per setup)."""
+    t = torch.tensor([state.boundary_max()], dtype=torch.int64,
+                     device=_coll_device(state.device))
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return int(t.item())
+
+
+def exchange_nccl(st: SlabState, group=None):
+    """First layer -> prev, last layer -> next, halos <- both, in one NCCL group.
+    Operations are posted in the same order on every rank, so NCCL's in-order
+    matching of point-to-point pairs is right even when prev == next (world 2,
+    periodic). Stream-ordered: the waits make the current stream wait."""
+    prv, nxt = st.plan.prev(st.rank), st.plan.next(st.rank)
+    if prv == st.rank:  # one rank on a periodic axis: its own opposite layers
+        return exchange_local([st])
+    ops = []
+    if prv is not None:
+        ops += [dist.P2POp(dist.isend, t, prv, group=group) for t in st.send(0)]
+    if nxt is not None:
+        ops += [dist.P2POp(dist.isend, t, nxt, group=group) for t in st.send(1)]
+    if nxt is not None:
+        ops += [dist.P2POp(dist.irecv, t, nxt, group=group) for t in st.recv(1)]
+    if prv is not None:
+        ops += [dist.P2POp(dist.irecv, t, prv, group=group) for t in st.recv(0)]
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+
+def exchange_gloo(st: SlabState, group=None):
+    """The same exchange staged through host memory over gloo (ranks sharing a
+    GPU, where NCCL cannot run): device -> host, tagged send/recv, host -> device."""
+    prv, nxt = st.plan.prev(st.rank), st.plan.next(st.rank)
+    if prv == st.rank:
+        return exchange_local([st])
+    works, inbox = [], []
+    for side, peer, tag in ((0, prv, 0), (1, nxt, 1)):
+        if peer is None:
+            continue
+        for i, t in enumerate(st.send(side)):
+            works.append(dist.isend(t.cpu(), peer, group=group, tag=16 * tag + i))
+    for side, peer, tag in ((1, nxt, 0), (0, prv, 1)):
+        if peer is None:
+            continue
+        for i, t in enumerate(st.recv(side)):
+            h = torch.empty(t.shape, dtype=t.dtype)
+            works.append(dist.irecv(h, peer, group=group, tag=16 * tag + i))
+            inbox.append((t, h))
+    for w in works:
+        w.wait()
+    for t, h in inbox:
+        t.copy_(h, non_blocking=False)
+
+
+def exchange_local(states):
+    """The same exchange between slabs held by one process (single-GPU tests)."""
+    by_rank = {st.rank: st for st in states}
+    for st in states:
+        plan, r = st.plan, st.rank
+        for side, peer, their in ((0, plan.prev(r), 1), (1, plan.next(r), 0)):
+            if peer is None:
+                continue
+            for dst, src in zip(st.recv(side), by_rank[peer].send(their)):
+                dst.copy_(src)
+
+
+# ---------------------------------------------------------------------------------------
+# owned particles of a rank
+# ---------------------------------------------------------------------------------------
+def _layers(ctx, grid, axis, pts, device):
+    """Global cell layer of each point (device binning on the global grid)."""
+    m = pts[0].numel()
+    rel = [torch.empty(m, dtype=torch.float64, device=device) for _ in range(grid.dim)]
+    cell = [torch.empty(m, dtype=torch.int32, device=device) for _ in range(grid.dim)]
+    cell_of = torch.empty(m, dtype=torch.int32, device=device)
+    start = torch.empty(grid.cell_total + 1, dtype=torch.int32, device=device)
+    items = torch.empty(m, dtype=torch.int32, device=device)
+    ctx.build_rel_coords_device(grid, pts, rel, cell, cell_of, start, items)
+    return cell[axis]
+
+
+def owned_from_host(ctx, grid, plan: SlabPlan, rank: int, x_host, device, chunk: int = 1 << 22):
+    """Owned particles of `rank` out of a host-resident global system (ascending ids)."""
     L0, L1 = plan.owned(rank)
     n = len(x_host[0])
-    xs, ids, lays = [[] for _ in range(grid.dim)], [], []
+    xs, ids = [[] for _ in range(grid.dim)], []
     for c0 in range(0, n, chunk):
         c1 = min(n, c0 + chunk)
-        m = c1 - c0
         xd = [torch.from_numpy(np.ascontiguousarray(a[c0:c1])).to(device) for a in x_host]
-        rel = [torch.empty(m, dtype=torch.float64, device=device) for _ in range(grid.dim)]
-        cell = [torch.empty(m, dtype=torch.int32, device=device) for _ in range(grid.dim)]
-        cell_of = torch.empty(m, dtype=torch.int32, device=device)
-        start = torch.empty(grid.cell_total + 1, dtype=torch.int32, device=device)
-        items = torch.empty(m, dtype=torch.int32, device=device)
-        ctx.build_rel_coords_device(grid, xd, rel, cell, cell_of, start, items)
-        lay = cell[plan.axis]
+        lay = _layers(ctx, grid, plan.axis, xd, device)
         keep = (lay >= L0) & (lay < L1)
         for k in range(grid.dim):
             xs[k].append(xd[k][keep])
         ids.append(torch.arange(c0, c1, dtype=torch.int32, device=device)[keep])
-        lays.append(lay[keep])
-    return [torch.cat(a) for a in xs], torch.cat(ids), torch.cat(lays)
+    return [torch.cat(a) for a in xs], torch.cat(ids)
 
 
-def global_table(slabs, n_global: int):
+def owned_lattice_device(ctx, grid, plan: SlabPlan, rank: int, sites, ds, lo, hi, device):
+    """Owned sites of an un-jittered lattice generated on the device
+    (sphx_lattice_device, bit-identical to build_lattice): only the planes around
+    the rank's layers are generated, then kept by their cell layer."""
+    dim, axis = grid.dim, plan.axis
+    L0, L1 = plan.owned(rank)
+    plane = int(np.prod([sites[k] for k in range(dim) if k != axis]))
+    per_layer = float(grid.hc[axis]) / (2.0 * ds / max(hi[k] - lo[k] for k in range(dim)))
+    p0 = max(int(np.floor(L0 * per_layer)) - 2, 0)
+    p1 = min(int(np.ceil(L1 * per_layer)) + 2, sites[axis])
+    xd = [torch.empty((p1 - p0) * plane, dtype=torch.float64, device=device) for _ in range(dim)]
+    ctx.lattice_device(dim, lo, hi, ds, p0 * plane, xd)
+    lay = _layers(ctx, grid, axis, xd, device)
+    keep = (lay >= L0) & (lay < L1)
+    ids = torch.arange(p0 * plane, p1 * plane, dtype=torch.int32, device=device)[keep]
+    if ids.numel():
+        first, last = int(ids[0]) // plane, int(ids[-1]) // plane
+        if (first == p0 and p0 > 0) or (last == p1 - 1 and p1 < sites[axis]):
+            raise RuntimeError("plane window too narrow for the rank's layers")
+    return [a[keep] for a in xd], ids
+
+
+def global_table(states, n_global: int):
     """Host CSR of the whole system from per-slab rows (rows placed by global id)."""
     lens = np.zeros(n_global, np.int64)
     parts = []
-    for s in slabs:
+    for s in states:
         off = s.offsets.cpu().numpy()
-        ids = s.ids_owned.cpu().numpy()
+        ids = s.ids[: s.n_own].cpu().numpy()
         lens[ids] = np.diff(off)
         parts.append((ids, off, s.out[: int(off[-1])].cpu().numpy()))
     offsets = np.zeros(n_global + 1, np.int64)
@@ -327,6 +378,95 @@ def global_table(slabs, n_global: int):
 
 
 # ---------------------------------------------------------------------------------------
+# parity (in the bench)
+# ---------------------------------------------------------------------------------------
+LATTICE_OFFSETS3 = [(a, b, c) for a in range(-2, 3) for b in range(-2, 3) for c in range(-2, 3)
+                    if 0 < a * a + b * b + c * c < 5.76]  # |v| < kh = 2.4 ds: 56 sites
+LATTICE_OFFSETS2 = [(a, b, 0) for a in range(-2, 3) for b in range(-2, 3)
+                    if 0 < a * a + b * b < 5.76]
+
+
+def lattice_total(sites) -> int:
+    offs = LATTICE_OFFSETS3 if len(sites) == 3 else LATTICE_OFFSETS2
+    return int(sum(np.prod([max(sites[k] - abs(v[k]), 0) for k in range(len(sites))],
+                           dtype=np.int64) for v in offs))
+
+
+def sampled_rows(st: SlabState, samples: int, seed: int):
+    n = st.n_own
+    rng = np.random.default_rng(seed)
+    idx = np.sort(rng.choice(n, size=min(samples, n), replace=False)) if n else np.zeros(0, int)
+    off = st.offsets.cpu().numpy()
+    out = st.out[: int(off[-1])].cpu().numpy()
+    return idx, [out[off[i]: off[i + 1]] for i in idx]
+
+
+def parity_lattice(st: SlabState, sites, samples=1000, seed=1):
+    """Sampled owned rows against the un-jittered lattice's closed form (the sites
+    within 2.4 ds, global ids)."""
+    dim = len(sites)
+    offs = LATTICE_OFFSETS3 if dim == 3 else LATTICE_OFFSETS2
+    idx, rows = sampled_rows(st, samples, seed + st.rank)
+    gid = st.ids[: st.n_own].cpu().numpy()
+    bad = 0
+    for i, row in zip(idx, rows):
+        g = int(gid[i])
+        c = [g % sites[0], (g // sites[0]) % sites[1] if dim > 1 else 0,
+             g // (sites[0] * sites[1]) if dim > 2 else 0]
+        exp = []
+        for v in offs:
+            q = [c[k] + v[k] for k in range(dim)]
+            if all(0 <= q[k] < sites[k] for k in range(dim)):
+                exp.append(q[0] + sites[0] * (q[1] + (sites[1] * q[2] if dim > 2 else 0)))
+        bad += int(not np.array_equal(row, np.array(sorted(exp), dtype=np.int32)))
+    return len(idx), bad
+
+
+def parity_oracle(st: SlabState, prec: int, samples=500, seed=1):
+    """Sampled owned rows against the oracle's rel_distance classification of every
+    CSR member of the 3^d local neighbour cells (rel_distance(...) < round_to(prec,
+    cutoff) <=> listed, test_nnps.cpp:158-184)."""
+    import oracle as O
+    orc = O.Oracle()
+    dim = st.dim
+    og = orc.grid(dim, st.grid.radius_phys, lo=list(st.grid.lo), hi=list(st.grid.hi),
+                  periodic=list(st.grid.periodic))
+    relh = [t.cpu().numpy() for t in st.rel]
+    cellh = [t.cpu().numpy() for t in st.cell]
+    start = st.start.cpu().numpy()
+    items = st.items.cpu().numpy()
+    ids = st.ids.cpu().numpy()
+    cnt = list(st.local.counts)[:dim]
+    per = [bool(st.local.periodic[k]) and cnt[k] > 2 for k in range(dim)]
+    cutoff = orc.round_to(prec, og.cutoff_norm)
+    idx, rows = sampled_rows(st, samples, seed + st.rank)
+    bad = 0
+    rng3 = [(-1, 0, 1) if k < dim else (0,) for k in range(3)]
+    for i, row in zip(idx, rows):
+        ci = [int(cellh[k][i]) for k in range(dim)]
+        exp = []
+        for dz in rng3[2]:
+            for dy in rng3[1]:
+                for dx in rng3[0]:
+                    c = [ci[k] + (dx, dy, dz)[k] for k in range(dim)]
+                    ok = True
+                    for k in range(dim):
+                        if not 0 <= c[k] < cnt[k]:
+                            if not per[k]:
+                                ok = False
+                            c[k] %= cnt[k]
+                    if not ok:
+                        continue
+                    lin = c[0] + (cnt[0] * (c[1] + (cnt[1] * c[2] if dim > 2 else 0)) if dim > 1 else 0)
+                    for p in range(start[lin], start[lin + 1]):
+                        j = int(items[p])
+                        if j != i and orc.rel_distance(og, relh, cellh, int(i), j, prec) < cutoff:
+                            exp.append(int(ids[j]))
+        bad += int(not np.array_equal(row, np.array(sorted(exp), dtype=np.int32)))
+    return len(idx), bad
+
+
+# ---------------------------------------------------------------------------------------
 # bench (N > 1 under torchrun)
 # ---------------------------------------------------------------------------------------
 def _env():
@@ -334,170 +474,182 @@ def _env():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def bench(args, workloads, metric, clock_sampler=None, peaks=(6650.0, "fallback"), golden=None):
-    """Weak scaling: the config's lattice stacked `world` times along the slab axis
-    (rank r owns about one config's worth of particles). A step is one rows() call
-    per rank on resident slab inputs (owned + halo RelCoords + local CSR), the
-    multi-GPU counterpart of the one-GPU step; the full per-call pipeline
-    (halo exchange + window binning + rows) is timed separately under "pipeline"."""
+def workload_sites(w, world: int, scaling: str):
+    """Global lattice sites per axis and the domain [0, hi] for `world` ranks. Weak
+    scaling stacks the per-GPU lattice (w["weak_sites"], else the whole config)
+    `world` times along the slab axis; strong splits the whole config."""
+    dim, ds = w["dim"], w["ds"]
+    side = [int(round(1.0 / ds))] * dim
+    if scaling == "weak" and "weak_sites" in w:
+        side = list(w["weak_sites"])
+    hi = [s * ds for s in side]
+    if scaling == "weak":
+        side[dim - 1] *= world
+        hi[dim - 1] *= world
+    return side, hi
+
+
+def bench(args, workloads, metric, clock_sampler=None, peaks=(6650.0, "fallback")):
+    """N ranks, one slab each. A step is one NNPS call per rank: the halo exchange
+    (NCCL, or host-staged gloo with --share-gpu), the slab assembly and the owned
+    rows, on resident owned RelCoords -- timed with CUDA events on the rank's
+    stream, the reported time the max over ranks of the median step."""
     world, rank, local = _env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if "RANK" not in os.environ:  # `bench.py --slab` without torchrun: a world of one
-        import socket
-        with socket.socket() as s:
-            s.bind(("127.0.0.1", 0))
-            port = s.getsockname()[1]
-        os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
-                          MASTER_PORT=str(port))
-    dist.init_process_group("nccl", device_id=dev)
+    share = bool(getattr(args, "share_gpu", False))
+    dev_index = 0 if share else local
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    if share:
+        dist.init_process_group("gloo")
+        exchange = exchange_gloo
+    else:
+        dist.init_process_group("nccl", device_id=dev)
+        exchange = exchange_nccl
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
     w = workloads[args.config]
+    scaling = args.scaling
     prec = {"fp64": 0, "fp32": 1, "fp16": 2}[args.precision]
     dim, ds = w["dim"], w["ds"]
     h = 1.2 * ds
-    hi = [1.0, 1.0, 1.0]
-    hi[dim - 1] = float(world)
-    x_host = capi.build_lattice(dim, ds, w["jitter"], w["seed"], lo=(0, 0, 0), hi=hi)
-    n_global = len(x_host[0])
-    grid = capi.grid_init(dim, (0, 0, 0), hi, 2.0 * h)
+    sites, hi = workload_sites(w, world, scaling)
+    lo = [0.0] * dim
+    grid = capi.grid_init(dim, (0, 0, 0), hi + [1.0] * (3 - dim), 2.0 * h)
     plan = SlabPlan.for_grid(grid, world)
-    ctx = capi.Context(local)
+    ctx = capi.Context(dev_index)
     ctx.set_stream(stream.cuda_stream)
 
-    xo, io, lay = owned_from_global(ctx, grid, plan, rank, x_host, dev)
-    del x_host
-    slab = Slab(ctx, grid, plan, rank, xo, io)
-    ex = lambda d, u: exchange_halo(plan, rank, d, u)  # noqa: E731
-    down, up = slab.boundary(layer_global=lay)
-    below, above = ex(down, up)
-    slab.assemble(below, above)
-    slab.bin()
-    total = slab.rows_sized(prec)
+    if w.get("device_lattice"):
+        xo, io = owned_lattice_device(ctx, grid, plan, rank, sites, ds, lo, hi, dev)
+    else:
+        x_host = capi.build_lattice(dim, ds, w["jitter"], w["seed"], lo=(0, 0, 0),
+                                    hi=tuple(hi) + (1.0,) * (3 - dim))
+        xo, io = owned_from_host(ctx, grid, plan, rank, x_host, dev)
+        del x_host
+    n_global = int(np.prod(sites))
+    st = SlabState(ctx, grid, plan, rank, xo, io)
+    del xo, io
+    st.allocate(agree_capacity(st) if world > 1 else st.boundary_max())
+    st.step(prec, exchange)
     torch.cuda.synchronize()
+    total = st.size_output(prec)
+    torch.cuda.synchronize()
+
+    # parity of this run: sampled rows (closed form / oracle) and the global total
+    if w.get("device_lattice") or w["jitter"] == 0.0:
+        checked, bad = parity_lattice(st, sites)
+        method = "sampled rows vs lattice closed form; total vs closed form"
+    else:
+        checked, bad = parity_oracle(st, prec)
+        method = "sampled rows vs oracle rel_distance classification of the 3^d cells"
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
-    ctx.enable_timing(True)
     for _ in range(args.warmup):
         flush.zero_()
-        slab.rows(prec)
+        st.step(prec, exchange)
     torch.cuda.synchronize()
     dist.barrier()
-
-    sampler = clock_sampler(local) if clock_sampler else None
+    sampler = clock_sampler(dev_index) if clock_sampler else None
     if sampler:
         sampler.__enter__()
     launches0 = ctx.launches
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    sweep_ms = []
     torch.cuda.synchronize()
     dist.barrier()
     for k in range(args.steps):
         flush.zero_()
         ev[k][0].record(stream)
-        slab.rows(prec)
+        st.step(prec, exchange)
         ev[k][1].record(stream)
-        sweep_ms.append(ctx.last_timing()[1])
     torch.cuda.synchronize()
-    dist.barrier()
     launches = ctx.launches - launches0
-    t_local = statistics.mean(a.elapsed_time(b) for a, b in ev) * 1e-3
-
-    # full per-call pipeline: exchange + window binning + rows
-    pipe_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(args.steps)]
-    ctx.enable_timing(False)
-    for _ in range(args.warmup):
-        slab.refresh(prec, ex)
-    torch.cuda.synchronize()
-    dist.barrier()
-    for k in range(args.steps):
+    t_local = statistics.median(a.elapsed_time(b) for a, b in ev) * 1e-3
+    # the rows alone (no exchange, no assembly), for the kernel's share of the step
+    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(max(args.steps // 2, 3))]
+    for a, b in ev2:
         flush.zero_()
-        pipe_ev[k][0].record(stream)
-        slab.refresh(prec, ex)
-        pipe_ev[k][1].record(stream)
+        a.record(stream)
+        st.rows(prec)
+        b.record(stream)
     torch.cuda.synchronize()
-    dist.barrier()
-    t_pipe_local = statistics.mean(a.elapsed_time(b) for a, b in pipe_ev) * 1e-3
+    t_rows_local = statistics.median(a.elapsed_time(b) for a, b in ev2) * 1e-3
 
-    # e2e: pinned host inputs -> H2D -> rows -> D2H of the table, per rank
-    h_in = [t[: slab.n].cpu().pin_memory() for t in slab.rel + slab.cell] + [
-        slab.items[: slab.n].cpu().pin_memory(), slab.start.cpu().pin_memory(),
-        slab.ids.cpu().pin_memory()]
-    d_in = [t[: slab.n] for t in slab.rel + slab.cell] + [slab.items[: slab.n], slab.start,
-                                                         slab.ids]
-    h_off = torch.empty(slab.n_owned + 1, dtype=torch.int64).pin_memory()
+    # e2e: the owned inputs from pinned host memory, the exchange, rows, the table back
+    h_in = [t[: st.n_own].cpu().pin_memory() for t in st.rel + st.cell] + [
+        st.ids[: st.n_own].cpu().pin_memory()]
+    d_in = [t[: st.n_own] for t in st.rel + st.cell] + [st.ids[: st.n_own]]
+    h_off = torch.empty(st.n_own + 1, dtype=torch.int64).pin_memory()
     h_out = torch.empty(max(total, 1), dtype=torch.int32).pin_memory()
     e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(args.e2e_steps)]
-    for k in range(args.e2e_steps):
-        e2e_ev[k][0].record(stream)
+              for _ in range(max(args.e2e_steps, 1))]
+    dist.barrier()
+    for a, b in e2e_ev:
+        a.record(stream)
         for hsrc, ddst in zip(h_in, d_in):
             ddst.copy_(hsrc, non_blocking=True)
-        slab.rows(prec)
-        h_off.copy_(slab.offsets, non_blocking=True)
-        h_out[:total].copy_(slab.out[:total], non_blocking=True)
-        e2e_ev[k][1].record(stream)
+        st.step(prec, exchange)
+        h_off.copy_(st.offsets, non_blocking=True)
+        h_out[:total].copy_(st.out[:total], non_blocking=True)
+        b.record(stream)
     torch.cuda.synchronize()
-    dist.barrier()
-    t_e2e_local = statistics.mean(a.elapsed_time(b) for a, b in e2e_ev) * 1e-3
+    t_e2e_local = statistics.median(a.elapsed_time(b) for a, b in e2e_ev) * 1e-3
     if sampler:
         sampler.__exit__(None, None, None)
 
-    red = torch.tensor([t_local, t_pipe_local, t_e2e_local], dtype=torch.float64, device=dev)
+    cdev = _coll_device(dev)
+    red = torch.tensor([t_local, t_rows_local, t_e2e_local], dtype=torch.float64, device=cdev)
     dist.all_reduce(red, op=dist.ReduceOp.MAX)
-    cnt = torch.tensor([slab.n_owned, total, launches, slab.n - slab.n_owned,
-                        sum(t.numel() * t.element_size() for t in h_in)],
-                       dtype=torch.int64, device=dev)
+    h2d_local = sum(t.numel() * t.element_size() for t in h_in)
+    halo_local = (st.cap * (8 * dim + 4) + 4 * (st.CL + 1)) * (int(st.has(0)) + int(st.has(1)))
+    cnt = torch.tensor([st.n_own, total, launches, checked, bad, h2d_local, halo_local],
+                       dtype=torch.int64, device=cdev)
     dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
-    t_max, t_pipe, t_e2e = red.tolist()
-    owned, pairs, launches_all, halo, h2d = [int(v) for v in cnt.tolist()]
-    # parity: one slab is the whole system, so its table must carry the reference's
-    # golden hash; with more slabs the stacked lattices have no reference table and
-    # tests/test_multigpu.py checks slab rows = one-GPU rows bit for bit
-    parity = {"checked": False,
-              "covered_by": "tests/test_multigpu.py (2/3/4 slabs, every precision: "
-                            "reassembled slab tables = the one-GPU table)"}
-    if world == 1 and golden is not None and args.config in ("C1", "C2", "C3"):
-        from .capi import table_hash
-        g = golden(args.config, args.precision)
-        h = table_hash(slab.offsets.cpu().numpy(), slab.out[:total].cpu().numpy())
-        parity = {"checked": True,
-                  "bit_exact_vs_reference_hash": total == g["total"] and f"{h:016x}" == g["hash"],
-                  "hash": f"{h:016x}", "golden": g["hash"]}
+    t_max, t_rows, t_e2e = red.tolist()
+    owned, pairs, launches_all, checked, bad, h2d, halo_bytes = [int(v) for v in cnt.tolist()]
+    closed = lattice_total(sites) if (w.get("device_lattice") or w["jitter"] == 0.0) else None
     if rank == 0:
         assert owned == n_global, (owned, n_global)
-        t_sweep = statistics.mean(sweep_ms) * 1e-3
         s_pos = {0: 8, 1: 4, 2: 2}[prec] * dim
-        n_l, C_l = slab.n, slab.local.cell_total
-        b_sweep = (n_l * s_pos + 4 * n_l + 4 * (C_l + 1) + 8 * (slab.n_owned + 1)
-                   + 4 * total)
+        C = grid.cell_total
+        b_sweep = (n_global * s_pos + 4 * n_global + 4 * (C + world) + 8 * (n_global + world)
+                   + 4 * pairs)
         peak, peak_kind = peaks
-        achieved = b_sweep / t_sweep / 1e9
+        achieved = b_sweep / world / t_rows / 1e9
+        parity = {"checked": True, "rows_checked": checked, "rows_differing": bad,
+                  "method": method,
+                  "bit_exact": bool(bad == 0 and (closed is None or closed == pairs))}
+        if closed is not None:
+            parity.update(total=pairs, total_expected=closed)
         line = {
             "metric": metric, "value": owned / t_max, "unit": "particles/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
             "dtype": {0: "f64", 1: "f32", 2: "f16"}[prec],
-            "data": "synthetic (reference build_lattice generator, seed 1, stacked per rank)",
-            "config": {"workload": f"{w['desc']} x{world} stacked along the slab axis",
-                       "n_particles": owned, "pairs": pairs, "halo_particles": halo,
+            "data": ("synthetic (lattice generated on the device per rank)"
+                     if w.get("device_lattice") else
+                     "synthetic (reference build_lattice generator, seed 1)"),
+            "config": {"workload": f"{w['desc']}, {scaling} scaling over {world} slab(s)",
+                       "sites": sites, "n_particles": owned, "pairs": pairs,
                        "precision": args.precision, "backend": "rcll",
                        "parallelism": f"slab{world} (cell layers along axis {plan.axis})",
+                       "exchange": ("host-staged gloo, ranks sharing one GPU" if share else
+                                    "NCCL p2p (grouped send/recv of the boundary layers)"),
+                       "halo_bytes_per_step": halo_bytes,
                        "l2": "flushed between timed steps (256 MiB write, outside the events)"},
             "parity": parity,
-            "pipeline": {"ms_per_step": t_pipe * 1e3, "value": owned / t_pipe,
-                         "what": "halo exchange (NCCL p2p) + window binning + rows"},
-            "roofline": {"bound": "hbm", "kernel": "k_rcll16 (2-D) / k_r16_test + k_r16_emit (3-D), rank 0",
+            "breakdown_ms": {"step": t_max * 1e3, "rows": t_rows * 1e3,
+                             "exchange_and_assembly": (t_max - t_rows) * 1e3},
+            "roofline": {"bound": "hbm", "kernel": "the rows of one rank (max over ranks)",
                          "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": None,
-                         "algorithmic_bytes": b_sweep},
+                         "algorithmic_bytes_per_rank": b_sweep / world},
             "e2e": {"value": owned / t_e2e, "unit": "particles/s", "ms_per_step": t_e2e * 1e3,
                     "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 8 * (owned + world) + 4 * pairs,
-                    "api": "pinned host slab inputs -> sphx_rcll_rows_device -> pinned table"},
+                    "api": "pinned host owned RelCoords -> exchange + assembly + rows -> "
+                           "pinned table"},
             "gpu_launches": launches_all,
             "clocks": sampler.summary() if sampler else None,
         }
