@@ -14,11 +14,11 @@
  *   sphx_all_list        <- NeighborTable all_list(const ParticleSystem&, Precision)
  *                                                                   nnps.hpp:31, nnps.cpp:128-172
  *   sphx_rebin           <- void CellGrid::rebin(const ParticleSystem&)
- *                                                                   cell_grid.hpp:147, cell_grid.cpp:66-108
+ *                                                                   cell_grid.hpp:86, cell_grid.cpp:66-108
  *   sphx_build_rel_coords<- RelCoords build_rel_coords(const ParticleSystem&, CellGrid&)
- *                                                                   cell_grid.hpp:181, cell_grid.cpp:114-133
+ *                                                                   cell_grid.hpp:120, cell_grid.cpp:114-133
  *   sphx_rebuild_members <- void CellGrid::rebuild_members(const RelCoords&)
- *                                                                   cell_grid.hpp:150, cell_grid.cpp:86-108
+ *                                                                   cell_grid.hpp:89, cell_grid.cpp:86-108
  *   sphx_table_copy      <- (ownership hand-off of the returned NeighborTable, nnps.hpp:16-26)
  *   sphx_update_relative(_device)
  *                        <- void update_relative(RelCoords&, size_t i, const std::array<double,3>&,
@@ -328,17 +328,6 @@ int sphx_lattice_device(sphx_context* ctx, int32_t dim, const double lo[3], cons
                         double ds, int64_t id0, int64_t count, double* const d_x[3]);
 
 /* ---------------- synthetic inputs ---------------- */
-/* build_gapped_random (experiments.cpp:55-112, anonymous namespace): the 2-D
- * guard-annulus generator of the paper's Table 2 accuracy workload (exp_square,
- * experiments.cpp:142-177). n particles drawn uniformly over [lo, hi] by dart
- * throwing, so that no pair distance falls within (cutoff - width, cutoff + width).
- * *ds_out = ParticleSystem's ds = (volume / n)^(1/2); x0/x1 = NULL is a ds query.
- * Host code (sequential by construction). SPHX_ERR_RUNTIME after 4000 rejected
- * draws of one particle, with the reference's message. */
-int sphx_build_gapped_random(const double lo[3], const double hi[3], int64_t n, double cutoff,
-                             double width, uint64_t seed, double* ds_out, double* x0, double* x1);
-
-
 /* build_lattice(Domain::box(dim, lo, hi), ds, jitter, seed) (particle_system.hpp:66,
  * particle_system.cpp:31-62): cell-centred lattice, x fastest, per-axis jitter
  * jitter*ds*(2u-1) from mt19937_64. Call with x0 == NULL to get *n only. */

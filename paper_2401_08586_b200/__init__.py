@@ -7,7 +7,7 @@ implementation, behind the C ABI in include/sphx_cuda.h (lib/libsphx_cuda.so).
 The C++ drop-in (include/sphx/*.hpp, module `_core`) sits on the same ABI.
 """
 from .capi import (FP16, FP32, FP64, PRECISIONS, Context, GridDesc, SphxCudaError,  # noqa: F401
-                   build_gapped_random, build_lattice, build_random_uniform, grid_init, lib)
+                   build_lattice, build_random_uniform, grid_init, lib)
 
 __all__ = ["FP16", "FP32", "FP64", "PRECISIONS", "Context", "GridDesc", "SphxCudaError",
-           "grid_init", "lib", "build_lattice", "build_random_uniform", "build_gapped_random"]
+           "grid_init", "lib", "build_lattice", "build_random_uniform"]

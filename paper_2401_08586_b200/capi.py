@@ -103,8 +103,6 @@ def lib():
                                                 p3, C.POINTER(i64)]),
         "sphx_rcll_grad_normalized_device": (C.c_int, [vp, G, i64, p3, p3, vp, vp, i32, p3, vp,
                                                        dbl, p3, vp]),
-        "sphx_build_gapped_random": (C.c_int, [C.POINTER(dbl), C.POINTER(dbl), i64, dbl, dbl, C.c_uint64,
-                                               C.POINTER(dbl), vp, vp]),
         "sphx_step_mixed_device": (C.c_int, [vp, G, i32, C.POINTER(MixedStateDevice),
                                              C.POINTER(StepConfig), vp, vp, i64,
                                              C.POINTER(dbl), C.POINTER(i64)]),
@@ -127,7 +125,7 @@ EXPORTED = ("sphx_last_error", "sphx_grid_init", "sphx_create", "sphx_destroy",
             "sphx_lattice_device", "sphx_rcll_distances_device", "sphx_table_distances",
             "sphx_rcll_grad_normalized", "sphx_rcll_grad_normalized_device",
             "sphx_update_relative", "sphx_update_relative_device", "sphx_rebuild_members_device",
-            "sphx_step_mixed_device", "sphx_build_gapped_random", "sphx_slab_assemble_device")
+            "sphx_step_mixed_device", "sphx_slab_assemble_device")
 
 APPROACH_I, APPROACH_II, APPROACH_III = 0, 1, 2
 
@@ -200,17 +198,6 @@ def build_random_uniform(dim: int, n: int, seed: int, lo=(0, 0, 0), hi=(1, 1, 1)
     check(lib().sphx_build_random_uniform(dim, _d3(lo), _d3(hi), n, seed, C.byref(ds),
                                           *[x.ctypes.data for x in xs], *([None] * (3 - dim))))
     return xs, ds.value
-
-
-def build_gapped_random(n: int, cutoff: float, width: float, seed: int, lo=(0, 0, 0),
-                        hi=(1, 1, 1)):
-    """build_gapped_random (experiments.cpp:55-112): 2-D positions with no pair
-    distance inside the guard annulus, and the ParticleSystem ds."""
-    x = [np.empty(n, np.float64) for _ in range(2)]
-    ds = C.c_double()
-    check(lib().sphx_build_gapped_random(_d3(lo), _d3(hi), n, float(cutoff), float(width), seed,
-                                         C.byref(ds), x[0].ctypes.data, x[1].ctypes.data))
-    return x, ds.value
 
 
 def _ptr3(arrs):

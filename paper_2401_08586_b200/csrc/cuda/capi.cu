@@ -366,6 +366,10 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
     return SPHX_OK;
   }
   const int64_t chunks = chunk_capacity(g.dim, prec, mode, n, C);
+  // record indices (selfpos) are 32-bit and chunk starts (xy_cstart) 31-bit
+  if (4 * chunks >= (int64_t(1) << 32) || chunks >= INT32_MAX)
+    return fail(SPHX_ERR_INVALID_ARGUMENT,
+                "too many candidate records for one context (split the system into slabs)");
   TRY(ctx->pos_own.ensure(coord_bytes(g.dim, prec) * (size_t)n));
   TRY(ctx->qc.ensure(chunk_bytes(g.dim, prec, mode) * (size_t)chunks));
   TRY(ctx->qtag.ensure(16 * (size_t)chunks));
@@ -1116,8 +1120,15 @@ int sphx_rcll_grad_normalized_device(sphx_context* ctx, const sphx_grid_desc* gr
     return fail(SPHX_ERR_INVALID_ARGUMENT,
                 "the fused gradient runs on the FP16 RCLL search in 2-D or 3-D");
   if (!(h > 0.0)) return fail(SPHX_ERR_INVALID_ARGUMENT, "smoothing length must be positive");
+  if (!d_degenerate) return fail(SPHX_ERR_INVALID_ARGUMENT, "null degenerate counter");
+  // GradField::degenerate_count is always written, 0 for an empty system (gradient.cpp:44-50)
+  CK(cudaMemsetAsync(d_degenerate, 0, sizeof(unsigned long long), ctx->stream));
   if (n == 0) return SPHX_OK;
   SweepArgs a;
+  // the fused search reuses the table scratch: a later sphx_table_copy /
+  // sphx_table_distances must not read it as the last rcll's table
+  ctx->t_n = -1;
+  ctx->t_rcll = false;
   TRY(ctx->t_offsets.ensure(sizeof(int64_t) * (n + 1)));
   TRY(run_prepare(ctx, MODE_RCLL, *grid, n, d_rel, d_cell, d_items, d_cell_start, nullptr,
                   precision, 0.0, ctx->t_offsets.as<int64_t>(), &a, RowSel(), false));
@@ -1131,7 +1142,6 @@ int sphx_rcll_grad_normalized_device(sphx_context* ctx, const sphx_grid_desc* gr
   // make_kernel (kernel.hpp:17-29), evaluated as the reference writes it
   const double pi = 3.141592653589793;
   a.galpha = grid->dim == 2 ? 15.0 / (7.0 * pi * h * h) : 3.0 / (2.0 * pi * h * h * h);
-  CK(cudaMemsetAsync(d_degenerate, 0, sizeof(unsigned long long), ctx->stream));
   ctx->launches += launch_rcll_grad(grid->dim, a, ctx->stream);
   CKL();
   if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], ctx->stream));
@@ -1352,66 +1362,6 @@ int sphx_build_lattice(int32_t dim, const double lo[3], const double hi[3], doub
         }
         ++idx;
       }
-  return SPHX_OK;
-}
-
-int sphx_build_gapped_random(const double lo[3], const double hi[3], int64_t n, double cutoff,
-                             double width, uint64_t seed, double* ds_out, double* x0, double* x1) {
-  // build_gapped_random (experiments.cpp:55-112): 2-D dart throwing with rejection;
-  // a candidate is redrawn while any placed particle lies at a distance within
-  // (cutoff - width, cutoff + width), searched over a bucket grid of edge
-  // cutoff + width. Sequential by construction (each draw depends on all earlier ones).
-  if (!ds_out || !lo || !hi) return fail(SPHX_ERR_INVALID_ARGUMENT, "null argument");
-  for (int k = 0; k < 2; ++k)
-    if (!(lo[k] < hi[k])) return fail(SPHX_ERR_INVALID_ARGUMENT, "domain bounds must satisfy lo < hi");
-  if (n <= 0) return fail(SPHX_ERR_INVALID_ARGUMENT, "particle count must be positive");
-  const double span0 = hi[0] - lo[0], span1 = hi[1] - lo[1];
-  *ds_out = std::pow(span0 * span1 / static_cast<double>(n), 0.5);  // ParticleSystem ds
-  if (!x0 || !x1) return SPHX_OK;
-  std::mt19937_64 gen(seed);
-  auto uniform = [&](double a, double b) {  // rng.hpp:15-17
-    return a + (b - a) * (static_cast<double>(gen() >> 11) * 0x1.0p-53);
-  };
-  const double lo2 = (cutoff - width) * (cutoff - width);
-  const double hi2 = (cutoff + width) * (cutoff + width);
-  const double bucket = cutoff + width;
-  const int bx = std::max(1, static_cast<int>(span0 / bucket));
-  const int by = std::max(1, static_cast<int>(span1 / bucket));
-  std::vector<std::vector<int32_t>> cells(static_cast<size_t>(bx) * by);
-  auto cell_of = [&](double x, double y, int& cx, int& cy) {
-    cx = std::min(std::max(static_cast<int>((x - lo[0]) / span0 * bx), 0), bx - 1);
-    cy = std::min(std::max(static_cast<int>((y - lo[1]) / span1 * by), 0), by - 1);
-  };
-  for (int64_t i = 0; i < n; ++i) {
-    for (int attempt = 0;; ++attempt) {
-      if (attempt > 4000)
-        return fail(SPHX_ERR_RUNTIME, "guard-annulus sampling stalled; widen the budget");
-      const double x = uniform(lo[0], hi[0]);
-      const double y = uniform(lo[1], hi[1]);
-      int cx, cy;
-      cell_of(x, y, cx, cy);
-      bool ok = true;
-      for (int oy = -1; oy <= 1 && ok; ++oy)
-        for (int ox = -1; ox <= 1 && ok; ++ox) {
-          const int qx = cx + ox, qy = cy + oy;
-          if (qx < 0 || qy < 0 || qx >= bx || qy >= by) continue;
-          for (const int32_t j : cells[static_cast<size_t>(qy) * bx + qx]) {
-            const double dx = x - x0[j], dy = y - x1[j];
-            const double d2 = dx * dx + dy * dy;
-            if (d2 > lo2 && d2 < hi2) {
-              ok = false;
-              break;
-            }
-          }
-        }
-      if (ok) {
-        x0[i] = x;
-        x1[i] = y;
-        cells[static_cast<size_t>(cy) * bx + cx].push_back(static_cast<int32_t>(i));
-        break;
-      }
-    }
-  }
   return SPHX_OK;
 }
 

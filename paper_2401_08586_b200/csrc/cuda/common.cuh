@@ -118,7 +118,7 @@ struct SlabArgs {
 // Look-back words carry flag and value in one 64-bit word, so relaxed gpu-scope
 // accesses suffice. (An acquire load would compile to CCTL.IVALL -- an L1
 // invalidation per spin iteration that evicts every warp's cached candidates.)
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
@@ -163,7 +163,7 @@ __device__ __forceinline__ long long lookback_exclusive(unsigned long long* tile
   // after a short sleep so that waiting warps do not steal issue slots
   while (true) {
     const int idx = p - lane;
-    const unsigned long long st = idx >= 0 ? ld_acquire_u64(&tiles[idx]) : PRE;
+    const unsigned long long st = idx >= 0 ? ld_relaxed_u64(&tiles[idx]) : PRE;
     const unsigned flag = (unsigned)(st >> 62);
     const unsigned pre_mask = __ballot_sync(0xffffffffu, flag == 2u);
     const unsigned zero_mask = __ballot_sync(0xffffffffu, flag == 0u);

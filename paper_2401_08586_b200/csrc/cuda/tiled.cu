@@ -571,7 +571,7 @@ __device__ __forceinline__ long long lb_resolve(unsigned long long* tiles, int b
   unsigned backoff = 32, spins = 0;
   while (true) {
     const int idx = p - lane;
-    const unsigned long long st = idx >= 0 ? ld_acquire_u64(&tiles[idx]) : (E | PRE);
+    const unsigned long long st = idx >= 0 ? ld_relaxed_u64(&tiles[idx]) : (E | PRE);
     const unsigned flag = (st >> 48) == epoch ? (unsigned)(st >> 46) & 3u : 0u;
     const unsigned pre_mask = __ballot_sync(0xffffffffu, flag == 2u);
     const unsigned zero_mask = __ballot_sync(0xffffffffu, flag == 0u);

@@ -41,7 +41,8 @@ NeighborTable all_list(const ParticleSystem& ps, Precision prec) {
   if (n == 0) throw std::invalid_argument("all_list needs at least one particle");
   const double* x[3] = {nullptr, nullptr, nullptr};
   for (int k = 0; k < ps.dim(); ++k) x[k] = ps.x(k).data();
-  sphx_context* ctx = cuda::context();
+  const cuda::Session session;  // held through the table copy
+  sphx_context* ctx = session.get();
   std::int64_t total = 0;
   cuda::check(sphx_all_list(ctx, ps.dim(), static_cast<std::int64_t>(n), x, ps.h(),
                             prec_code(prec), &total));
@@ -58,7 +59,8 @@ NeighborTable cell_link_list(const ParticleSystem& ps, const CellGrid& grid, Pre
   const double* x[3] = {nullptr, nullptr, nullptr};
   for (int k = 0; k < ps.dim(); ++k) x[k] = ps.x(k).data();
   const sphx_grid_desc g = cuda::describe(grid);
-  sphx_context* ctx = cuda::context();
+  const cuda::Session session;  // held through the table copy
+  sphx_context* ctx = session.get();
   std::int64_t total = 0;
   cuda::check(sphx_cell_link_list(ctx, &g, static_cast<std::int64_t>(n), x, ps.h(),
                                   static_cast<std::int64_t>(items.size()), items.data(),
@@ -79,7 +81,8 @@ NeighborTable rcll(const RelCoords& rc, const CellGrid& grid, Precision prec) {
     cell[k] = rc.cell[k].data();
   }
   const sphx_grid_desc g = cuda::describe(grid);
-  sphx_context* ctx = cuda::context();
+  const cuda::Session session;  // held through the table copy
+  sphx_context* ctx = session.get();
   std::int64_t total = 0;
   cuda::check(sphx_rcll(ctx, &g, static_cast<std::int64_t>(n), rel, cell,
                         static_cast<std::int64_t>(items.size()), items.data(),

@@ -15,18 +15,21 @@ struct Holder {
   }
 };
 
+std::recursive_mutex& session_mutex() {
+  static std::recursive_mutex mu;
+  return mu;
+}
+
 }  // namespace
 
-sphx_context* context() {
+Session::Session() : lock_(session_mutex()), ctx_(nullptr) {
   static Holder holder;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lock(mu);
   if (!holder.ctx) {
     int device = -1;
     if (const char* env = std::getenv("SPHX_DEVICE")) device = std::atoi(env);
     check(sphx_create(device, &holder.ctx));
   }
-  return holder.ctx;
+  ctx_ = holder.ctx;
 }
 
 void rethrow(int code) {

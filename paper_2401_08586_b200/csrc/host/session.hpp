@@ -5,6 +5,7 @@
 // compiles against the reference's own sphx headers as well as ours.
 #pragma once
 
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -14,9 +15,21 @@
 namespace sphx::cuda {
 
 // The library context used by the free functions (created on first use on the
-// current CUDA device; SPHX_DEVICE=<n> picks another). Throws std::runtime_error
-// when no sm_100 device is available -- there is no CPU fallback.
-sphx_context* context();
+// current CUDA device; SPHX_DEVICE=<n> picks another), held for the lifetime of
+// a Session: the context's staging and table buffers are shared, so each
+// drop-in call keeps it locked from its first C-ABI call through the table copy
+// (the reference's functions are reentrant; concurrent callers serialise here).
+// Throws std::runtime_error when no sm_100 device is available -- there is no
+// CPU fallback.
+class Session {
+ public:
+  Session();
+  sphx_context* get() const { return ctx_; }
+
+ private:
+  std::unique_lock<std::recursive_mutex> lock_;
+  sphx_context* ctx_;
+};
 
 // Rethrows a non-OK status as the reference's exception type with its message.
 [[noreturn]] void rethrow(int code);

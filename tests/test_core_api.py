@@ -424,3 +424,29 @@ def test_dropin_reference_library_gives_identical_tables(case):
             a = getattr(ref, be)(p)
             b = getattr(dr, be)(p)
             assert np.array_equal(a.offsets, b.offsets) and np.array_equal(a.items, b.items), (be, p)
+
+
+@pytest.mark.gpu
+def test_concurrent_calls_from_threads():
+    """The drop-in releases the GIL; concurrent rcll / cell_link_list / rebin calls
+    from several threads share one library context and must each return their own
+    table (the session lock holds the context through the table copy)."""
+    from concurrent.futures import ThreadPoolExecutor
+    systems = []
+    for s in range(6):
+        ps = c.build_lattice(c.Domain.unit(2), 0.01 + 0.002 * s, 0.3, 40 + s)
+        g = c.make_grid_for(ps)
+        rc = c.build_rel_coords(ps, g)
+        systems.append((ps, g, rc))
+    want = [(c.rcll(rc, g, F16), c.cell_link_list(ps, g, F32)) for ps, g, rc in systems]
+
+    def work(k):
+        ps, g, rc = systems[k % len(systems)]
+        g2 = c.make_grid_for(ps)
+        g2.rebin(ps)
+        a, b = c.rcll(rc, g, F16), c.cell_link_list(ps, g2, F32)
+        wa, wb = want[k % len(systems)]
+        return c.tables_equal(a, wa) and c.tables_equal(b, wb)
+
+    with ThreadPoolExecutor(max_workers=6) as ex:
+        assert all(ex.map(work, range(36)))

@@ -4,10 +4,10 @@ build_gapped_random (experiments.cpp:55-112) draws 2-D particles so that no pair
 distance lies within +-gap_rel*cutoff of the cutoff; exp_square (experiments.cpp:
 142-177) then compares the FP16 tables with the FP64 one, and the reference's own
 test asserts that FP16 RCLL has zero incorrect pairs on this data (the paper's
-Table 2 claim). The generator is host code in the library
-(sphx_build_gapped_random); the experiments TU cannot be compiled here (boost,
-nlohmann), so the generator is checked against the oracle's brute-force
-restatement (so_build_gapped_random), and the tables against the pinned oracle.
+Table 2 claim). The generator is a test workload, not part of the search path:
+it lives in the oracle (so_build_gapped_random, a brute-force restatement -- the
+experiments TU cannot be compiled here: boost, nlohmann), and the GPU tables on
+its output are checked against the reference's claim and the pinned oracle.
 """
 import numpy as np
 import pytest
@@ -27,16 +27,18 @@ def _rung(ds):
 RUNGS = [(0.05, 10), (0.02, 11), (0.01, 2)]
 
 
+def _gapped(n, cutoff, seed):
+    x = O.Oracle().gapped_random(n, cutoff, GAP_REL * cutoff, seed)
+    return x, 1.0 / np.sqrt(n)  # ParticleSystem ds = (volume / n)^(1/2) on the unit square
+
+
 @pytest.mark.parametrize("ds,seed", RUNGS)
-def test_generator_matches_oracle_and_keeps_the_annulus_empty(ds, seed):
-    import paper_2401_08586_b200 as P
+def test_generator_is_deterministic_and_keeps_the_annulus_empty(ds, seed):
     n, cutoff = _rung(ds)
-    x, ds_ps = P.build_gapped_random(n, cutoff, GAP_REL * cutoff, seed)
-    want = O.Oracle().gapped_random(n, cutoff, GAP_REL * cutoff, seed)
-    assert all(np.array_equal(x[k], want[k]) for k in range(2))
-    assert ds_ps == pytest.approx(1.0 / np.sqrt(n), rel=1e-15)
-    again, _ = P.build_gapped_random(n, cutoff, GAP_REL * cutoff, seed)
+    x, _ = _gapped(n, cutoff, seed)
+    again, _ = _gapped(n, cutoff, seed)
     assert all(np.array_equal(x[k], again[k]) for k in range(2))
+    assert all(((0.0 <= a) & (a <= 1.0)).all() for a in x)
     if n <= 2500:
         d2 = (x[0][:, None] - x[0][None, :]) ** 2 + (x[1][:, None] - x[1][None, :]) ** 2
         lo2, hi2 = (cutoff * (1 - GAP_REL)) ** 2, (cutoff * (1 + GAP_REL)) ** 2
@@ -44,9 +46,8 @@ def test_generator_matches_oracle_and_keeps_the_annulus_empty(ds, seed):
 
 
 def test_generator_stall_error():
-    import paper_2401_08586_b200 as P
     with pytest.raises(RuntimeError, match="guard-annulus sampling stalled; widen the budget"):
-        P.build_gapped_random(2000, 0.3, 0.29, 1)
+        O.Oracle().gapped_random(2000, 0.3, 0.29, 1)
 
 
 @pytest.mark.gpu
@@ -55,7 +56,7 @@ def test_fp16_rcll_is_exact_on_guard_annulus_data(ds, seed):
     import paper_2401_08586_b200 as P
     ctx = P.Context(0)
     n, cutoff = _rung(ds)
-    x, ds_ps = P.build_gapped_random(n, cutoff, GAP_REL * cutoff, seed)
+    x, ds_ps = _gapped(n, cutoff, seed)
     h = 1.2 * ds_ps  # ParticleSystem h of exp_square's system
     orc = O.Oracle()
     og = orc.grid(2, 2.0 * h)
