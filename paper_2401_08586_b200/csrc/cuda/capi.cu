@@ -48,6 +48,9 @@ void launch_lattice(int dim, const double lo[3], double ds, const int64_t counts
                     int64_t count, double* const x[3], cudaStream_t st);
 int launch_step_rates(int dim, const StepArgs& a, cudaStream_t st);
 int launch_kick_drift(int dim, const StepArgs& a, cudaStream_t st);
+// window.cu
+int64_t win2_tiles(int64_t nrows);
+int launch_win2(const Win2Args& a, cudaStream_t st);
 // tiled.cu
 void tiled2_shape(int nx, int ny, int64_t n, int* tw, int* tpr, int64_t* ntiles);
 int64_t tiled2_scan_tiles(int64_t nrows);
@@ -153,6 +156,8 @@ struct sphx_context {
   Buf s_stress, s_rates, s_dx, s_flags;
   // cell-tiled 2-D FP16 RCLL: row lengths, hit words, per-row path flags
   Buf tl_cnt, tl_mw, tl_mx, tl_flag, tl_rank;
+  // windowed 2-D FP16 RCLL: CSR-order binary16 x/y pairs, cell x, ids, run lists
+  Buf w_xy, w_u, w_id, w_run;
 };
 
 namespace {
@@ -319,6 +324,13 @@ bool tiled2_enabled() {
   return e && e[0] == '1';
 }
 
+// The windowed 2-D FP16 RCLL path (window.cu) is the default; SPHX_W2=0 selects
+// the encode + k_rcll16 path.
+bool win2_enabled() {
+  const char* e = std::getenv("SPHX_W2");
+  return !(e && e[0] == '0');
+}
+
 int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n64,
                 const double* const src[3], const int32_t* const cellk[3], const int32_t* items,
                 const int32_t* start, const int32_t* cell_of, int prec, double h, int64_t* d_off,
@@ -342,6 +354,33 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
     return SPHX_OK;
   }
   const int64_t C = mode == MODE_ALL ? 0 : cell_total(g);
+  if (allow_tiled && g.dim == 2 && prec == SPHX_FP16 && mode == MODE_RCLL && !sel.ids &&
+      g.counts[0] <= 2048 && win2_enabled() && !tiled2_enabled()) {
+    const PrecConsts pc = make_consts(mode, prec, g, h);
+    if (pc.h_thr != 0) {  // (thr == 0: no pair can hit; the generic path handles it)
+      // windowed path (window.cu): pack + sweep in run_sweep, no encode
+      const size_t np = (size_t)n + 64;
+      TRY(ctx->w_xy.ensure(4 * np));
+      TRY(ctx->w_u.ensure(2 * np));
+      TRY(ctx->w_id.ensure(4 * np));
+      TRY(ctx->w_run.ensure(32 * (size_t)C));
+      SweepArgs& a = *out;
+      a.g = grid_consts(g);
+      a.c = pc;
+      a.win2 = 1;
+      for (int k = 0; k < 3; ++k) {
+        a.src[k] = k < g.dim ? src[k] : nullptr;
+        a.cellk[k] = cellk ? cellk[k] : nullptr;
+      }
+      a.start = start;
+      a.cell_of = cell_of;
+      if (ctx->timing) {
+        CK(cudaEventRecord(ctx->ev[0], st));
+        CK(cudaEventRecord(ctx->ev[1], st));
+      }
+      return SPHX_OK;
+    }
+  }
   if (allow_tiled && g.dim == 2 && prec == SPHX_FP16 && mode == MODE_RCLL && tiled2_enabled()) {
     // the cell-tiled path (tiled.cu): no encode, count -> scan -> fill in run_sweep
     TRY(ctx->tl_cnt.ensure(sizeof(int32_t) * (size_t)nrows));
@@ -412,8 +451,9 @@ int run_sweep(sphx_context* ctx, int dim, int prec, int mode, SweepArgs& a, int3
               int64_t capacity) {
   if (a.n == 0 || a.nrows == 0) return SPHX_OK;
   cudaStream_t st = ctx->stream;
-  const int64_t nt = a.tiled ? tiled2_scan_tiles(a.nrows)
-                             : (a.nrows + sweep_tile(dim, prec, mode) - 1) / sweep_tile(dim, prec, mode);
+  const int64_t nt = a.win2    ? win2_tiles(a.nrows)
+                     : a.tiled ? tiled2_scan_tiles(a.nrows)
+                               : (a.nrows + sweep_tile(dim, prec, mode) - 1) / sweep_tile(dim, prec, mode);
   if (nt > ctx->sw_ntiles || ctx->sw_epoch >= 0xFFFFu) {
     // fresh (or recycled) look-back words: epoch 0 marks them unpublished
     TRY(ctx->sw_tiles.ensure(sizeof(unsigned long long) * std::max<int64_t>(nt, ctx->sw_ntiles)));
@@ -425,6 +465,34 @@ int run_sweep(sphx_context* ctx, int dim, int prec, int mode, SweepArgs& a, int3
     TRY(ctx->sw_ticket.ensure(sizeof(unsigned long long)));
     CK(cudaMemsetAsync(ctx->sw_ticket.p, 0, sizeof(unsigned long long), st));
     ctx->sw_tick = 0;
+  }
+  if (a.win2) {
+    Win2Args w;
+    std::memset(&w, 0, sizeof(w));
+    w.n = a.n;
+    w.row0 = a.row0;
+    w.nrows = a.nrows;
+    w.g = a.g;
+    w.c = a.c;
+    for (int k = 0; k < 2; ++k) {
+      w.rel[k] = a.src[k];
+      w.cellk[k] = a.cellk[k];
+    }
+    w.items = a.order;
+    w.start = a.start;
+    w.wxy = ctx->w_xy.as<__half>();
+    w.wu = ctx->w_u.as<__half>();
+    w.wid = ctx->w_id.as<int32_t>();
+    w.wrun = ctx->w_run.as<uint8_t>();
+    w.offsets = a.offsets;
+    w.out = d_items;
+    w.capacity = capacity;
+    w.tiles = ctx->sw_tiles.as<unsigned long long>();
+    w.epoch = ++ctx->sw_epoch;
+    ctx->launches += launch_win2(w, st);
+    CKL();
+    if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], st));
+    return SPHX_OK;
   }
   if (a.tiled) {
     TileArgs t;

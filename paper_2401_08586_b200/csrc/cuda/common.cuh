@@ -68,6 +68,7 @@ struct SweepArgs {
   int32_t* rowk;              // [nrows] row lengths of the test pass (bit 31: words overflowed)
   unsigned* hitw;             // [W][nrows] hit words of the test pass
   int tiled;                  // 2-D FP16 RCLL: the cell-tiled path (tiled.cu), no encode
+  int win2;                   // 2-D FP16 RCLL: the windowed path (window.cu), no encode
   const double* src[3];       // tiled path: RelCoords::rel[k]
   const int32_t* start;       // tiled path: CellGrid::cell_start
 };
@@ -97,6 +98,27 @@ struct TileArgs {
   int32_t* out;               // [capacity] neighbour ids
   int64_t capacity;
   unsigned long long* tiles;  // scan look-back words (epoch-tagged)
+  unsigned epoch;
+};
+
+// Arguments of the windowed 2-D FP16 RCLL (capi.cu fills them).
+struct Win2Args {
+  int n;                      // particles (CSR size)
+  int row0, nrows;            // rows produced: particles [row0, row0 + nrows)
+  GridConsts g;
+  PrecConsts c;
+  const double* rel[2];       // RelCoords::rel[k] (particle order)
+  const int32_t* cellk[2];    // RelCoords::cell[k]
+  const int32_t* items;       // CellGrid::items (CSR)
+  const int32_t* start;       // CellGrid::cell_start [C+1]
+  __half* wxy;                // [n + 16] pair-interleaved binary16 x / y (CSR order)
+  __half* wu;                 // [n + 16] CSR cell x of each record (binary16)
+  int32_t* wid;               // [n + 16] candidate ids (CSR order)
+  uint8_t* wrun;              // [C][32] run lists: positions of each x-triple in id order
+  int64_t* offsets;           // [nrows + 1]
+  int32_t* out;               // [capacity]
+  int64_t capacity;
+  unsigned long long* tiles;  // look-back words (epoch-tagged, never cleared)
   unsigned epoch;
 };
 

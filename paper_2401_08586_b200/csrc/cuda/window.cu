@@ -1,0 +1,781 @@
+// Windowed FP16 RCLL for 2-D -- the BASELINE metric path: rcll(rel, grid, fp16)
+// of nnps.cpp:283-416 (2-D FP16: the batch kernel detail::range_f16_rel_2d,
+// nnps_batch.cpp:203-261) with build_table's sorted rows (nnps.cpp:26-66).
+//
+// Two kernels per call, chained with programmatic dependent launch:
+//
+//   k_w2_pack   the reference's per-call preparation (nnps.cpp:300-315), in CSR
+//               order. Record blocks: xy[4p + (s&1)] = r16(rel_x[items[s]]),
+//               xy[4p + 2 + (s&1)] = r16(rel_y[...]) (p = s/2: one 8-byte load
+//               is the x pair and the y pair of two neighbouring records) and
+//               id[s] = items[s]. Cell blocks (one thread per cell v):
+//               u[s] = x(v) as binary16 for v's members (the CSR cell, so
+//               u_i - u_j is the reference's minimum-image dc = -off,
+//               nnps.cpp:359-362; exact: the path needs nx <= 2048), and the
+//               *run list* of the x-triple centred at v: the positions of cells
+//               v-1, v, v+1 (one contiguous CSR span) in ascending id order, by a
+//               3-way merge of the cells' ascending ids (32 bytes, 0xFF-padded).
+//
+//   k_w2<BT>    one CTA per tile of BT consecutive rows (particle order). The
+//               tile's targets are split at id-order jumps of more than two
+//               cells into at most two *bands*; each band's window -- cell rows
+//               ymin-1 .. ymax+1, cells xmin-1 .. xmax+1 -- is one contiguous CSR
+//               range per cell row (linear cell = cx + nx*cy, x fastest,
+//               cell_grid.hpp:74-78), staged in shared memory with TMA bulk
+//               copies (cp.async.bulk, one mbarrier) together with the run lists
+//               of its centre cells. A target's candidates in stencil row oy are
+//               one contiguous window segment (cells cx-1, cx, cx+1):
+//               A  tested two per binary16x2 op straight from shared memory
+//                  (warp-uniform trip count, dc = u_i - u_j as one HSUB2) into a
+//                  32-bit hit word per segment; the target's own record is found
+//                  by id in its cell and cleared; block scan; decoupled look-back
+//                  publish;
+//               B  the centre cell's run list walks the segment in id order, so
+//                  hits are appended already sorted (a segment whose ids
+//                  interleave with the previous row's is merged in); rows packed
+//                  in shared memory (over the dead coordinates), 16-byte stores.
+//
+// Tiles whose targets do not form <= 2 compact bands (a shuffled particle order),
+// whose window exceeds shared memory or wraps a periodic x axis, and targets whose
+// segment exceeds 32 positions or whose RelCoords cell is not their CSR cell take
+// an exact per-row path that walks the 9 cells in global memory like the
+// reference (nnps.cpp:354-410) and sorts the row.
+//
+// Exactness (per candidate, nnps.cpp:332-346, nnps_batch.cpp:238-258):
+// s = r16(ri - rj); t = r16(s*hh); x: d = r16(t + r16(dc*hc)) as one HFMA2 (dc in
+// {-1,0,1}, dc*hc16 exact); y: d = r16(t + cc) (cc = r16(-oy*hc); skipped in the
+// centre row, where t + 0 only turns -0 into +0, which squares the same);
+// acc = r16(r16(dx^2) + r16(dy^2)); hit iff acc < thr, the exact threshold of
+// r16(sqrt(acc)) < cutoff16 (capi.cu thr16).
+
+#include <climits>
+#include <cstdlib>
+#include <utility>
+
+#include "common.cuh"
+
+namespace sphx_dev {
+
+namespace {
+
+constexpr int kSegMax = 32;   // positions per segment (one hit word, one run list)
+constexpr int kRowsMax = 12;  // window rows (both bands)
+constexpr int kBandRows = 6;  // rows of one band: ymax - ymin <= 3
+constexpr int kPackR = 4;     // records per pack thread
+
+template <int BT>
+struct W2Cfg {
+  static constexpr int WCap = 12 * BT + BT / 2;  // window records
+  static constexpr int PCap = WCap * 3 / 2;      // packed row entries (alias the coordinates)
+  static constexpr int CSCap = 4 * BT;           // window cell boundaries
+  static constexpr int RunCap = 7 * BT / 4;      // run lists
+  static constexpr int MinB = 1024 / BT;         // CTAs per SM (register budget)
+};
+
+__device__ __forceinline__ unsigned h2u(__half2 h) { return *reinterpret_cast<const unsigned*>(&h); }
+__device__ __forceinline__ __half2 u2h(unsigned u) { return *reinterpret_cast<const __half2*>(&u); }
+__device__ __forceinline__ __half hb(unsigned b) { return __ushort_as_half((unsigned short)b); }
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// bits [q, 32) set
+__device__ __forceinline__ unsigned above(int q) { return q >= 32 ? 0u : ~0u << q; }
+
+// y centre difference of stencil row oy: cc = r16(dc*hc) with dc = -oy
+__device__ __forceinline__ __half cc_half(unsigned hc16, int oy) {
+  return oy == 0 ? hb(0) : hb(oy < 0 ? hc16 : (hc16 ^ 0x8000u));
+}
+
+struct SharedRow {
+  uint32_t base;
+  __device__ __forceinline__ void st(int e, int v) const {
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(base + 4u * (uint32_t)e), "r"(v) : "memory");
+  }
+  __device__ __forceinline__ int ld(int e) const {
+    int v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(base + 4u * (uint32_t)e) : "memory");
+    return v;
+  }
+};
+struct GlobalRow {
+  int32_t* p;
+  __device__ __forceinline__ void st(int e, int v) const { p[e] = v; }
+  __device__ __forceinline__ int ld(int e) const { return p[e]; }
+};
+
+// dst[0, gs) and dst[gs, k) are each sorted: insert the tail into the head
+// (stops at the first tail element already above everything before it).
+template <class Row>
+__device__ __forceinline__ void merge_tail(const Row& dst, int gs, int k) {
+  for (int e = gs; e < k; ++e) {
+    const int v = dst.ld(e);
+    int w = dst.ld(e - 1);
+    if (w < v) break;
+    int q = e;
+    do {
+      dst.st(q, w);
+      --q;
+    } while (q > 0 && (w = dst.ld(q - 1)) > v);
+    dst.st(q, v);
+  }
+}
+
+template <class Row>
+__device__ __forceinline__ void insertion_sort(const Row& dst, int k) {
+  for (int e = 1; e < k; ++e) {
+    const int v = dst.ld(e);
+    int q = e;
+    int w;
+    while (q > 0 && (w = dst.ld(q - 1)) > v) {
+      dst.st(q, w);
+      --q;
+    }
+    dst.st(q, v);
+  }
+}
+
+// look-back words: [63:48] epoch, [47:46] flag (1 aggregate, 2 inclusive), [45:0] value
+__device__ __forceinline__ void lb_publish(unsigned long long* tiles, int bid, long long total,
+                                           unsigned epoch) {
+  const unsigned long long E = (unsigned long long)epoch << 48;
+  st_release_u64(&tiles[bid], E | ((bid == 0 ? 2ull : 1ull) << 46) | (unsigned long long)total);
+}
+
+__device__ __forceinline__ long long lb_resolve(unsigned long long* tiles, int bid, long long total,
+                                                unsigned epoch) {
+  if (bid == 0) return 0;
+  const unsigned long long E = (unsigned long long)epoch << 48, PRE = 2ull << 46,
+                           VAL = (1ull << 46) - 1;
+  const int lane = threadIdx.x & 31;
+  long long excl = 0;
+  int p = bid - 1;
+  unsigned backoff = 64, spins = 0;
+  while (true) {
+    const int idx = p - lane;
+    const unsigned long long st = idx >= 0 ? ld_relaxed_u64(&tiles[idx]) : (E | PRE);
+    const unsigned flag = (st >> 48) == epoch ? (unsigned)(st >> 46) & 3u : 0u;
+    const unsigned pre_mask = __ballot_sync(0xffffffffu, flag == 2u);
+    const unsigned zero_mask = __ballot_sync(0xffffffffu, flag == 0u);
+    const int first = pre_mask ? __ffs(pre_mask) - 1 : 32;
+    const unsigned need = first >= 31 ? 0xffffffffu : ((2u << first) - 1u);
+    if (zero_mask & need) {
+      // tiles run in blockIdx order, so a predecessor that never publishes is a
+      // bug: fail the launch (~4 s) instead of hanging the device
+      if (++spins > (1u << 22)) __trap();
+      __nanosleep(backoff);
+      backoff = backoff < 1024 ? backoff * 2 : 1024;
+      continue;
+    }
+    const long long v = lane <= first ? (long long)(st & VAL) : 0ll;
+    excl += warp_sum_ll(v);
+    if (first < 32) break;
+    p -= 32;
+  }
+  if (lane == 0) st_release_u64(&tiles[bid], E | PRE | (unsigned long long)(excl + total));
+  return excl;
+}
+
+template <int BT>
+__device__ __forceinline__ void stream_tile(int32_t* gout, const SharedRow& pk, int n, int tid) {
+  const int ph = (int)(((uintptr_t)gout & 15u) >> 2);
+  int4* g4 = reinterpret_cast<int4*>(gout - ph);
+  const int nv = (ph + n + 3) >> 2;
+  for (int q = tid; q < nv; q += BT) {
+    const int e0 = 4 * q - ph;
+    if (e0 >= 0 && e0 + 4 <= n) {
+      g4[q] = make_int4(pk.ld(e0), pk.ld(e0 + 1), pk.ld(e0 + 2), pk.ld(e0 + 3));
+    } else {
+      for (int e = max(e0, 0); e < min(e0 + 4, n); ++e) gout[e] = pk.ld(e);
+    }
+  }
+}
+
+// One candidate pair (positions 2t, 2t+1 of a segment): hits set the bits
+// `bit` and `bit << 1` of H.
+__device__ __forceinline__ void pair_test(unsigned X2, unsigned Y2, unsigned U2, __half2 rx2,
+                                          __half2 ry2, __half2 ut2, __half2 hhx, __half2 hhy,
+                                          __half2 hc2, __half2 ccy, bool ycc, __half2 thr2,
+                                          unsigned bit, unsigned& H) {
+  const __half2 tx = __hmul2_rn(__hsub2_rn(rx2, u2h(X2)), hhx);
+  const __half2 dx = __hfma2(__hsub2_rn(ut2, u2h(U2)), hc2, tx);
+  __half2 ty = __hmul2_rn(__hsub2_rn(ry2, u2h(Y2)), hhy);
+  if (ycc) ty = __hadd2_rn(ty, ccy);
+  const __half2 acc = __hadd2_rn(__hmul2_rn(dx, dx), __hmul2_rn(ty, ty));
+  asm("{\n\t.reg .pred p0, p1;\n\t"
+      ".reg .b32 b1;\n\t"
+      "setp.lt.f16x2 p0|p1, %1, %2;\n\t"
+      "shl.b32 b1, %3, 1;\n\t"
+      "@p0 or.b32 %0, %0, %3;\n\t"
+      "@p1 or.b32 %0, %0, b1;\n\t}"
+      : "+r"(H)
+      : "r"(h2u(acc)), "r"(h2u(thr2)), "r"(bit));
+}
+
+template <int BT>
+struct W2Smem {
+  using C = W2Cfg<BT>;
+  union {
+    struct {
+      uint2 xy[C::WCap / 2 + 16];  // pair p: {x pair, y pair} of positions 2p, 2p+1 (+ pad:
+      __half u[C::WCap + 32];      //   idle lanes read up to 32 positions past a segment)
+    } c;
+    int pk[C::PCap];               // phase B: the tile's packed rows (the coordinates are dead)
+  };
+  int id[C::WCap];                 // candidate particle ids
+  uint4 run[C::RunCap * 2];        // run lists of the window's centre cells (32 bytes each)
+  short cs[C::CSCap];              // window cell boundaries, relative to the row's CSR start
+  unsigned hw[3][BT];              // phase A hit words of the 3 segments
+  int rbase[kRowsMax];             // row r: window position of its first record
+  int ra8[kRowsMax], rn[kRowsMax]; //   aligned CSR start (-1: no row), records
+  int rgy[kRowsMax];               //   grid row
+  int bx[2][4];                    // band: xmin, xmax, ymin, ymax
+  int last[BT / 32][2];            // warp w's lane 31 cell (x, y)
+  int wsum[BT / 32];
+  int split, total;
+  long long base;
+  unsigned long long bar;
+};
+
+// Band geometry (identical in every thread: computed from S.bx).
+struct Geo {
+  int rows[2], ncs[2], nrun[2];
+  __device__ __forceinline__ int row0(int q) const { return q ? rows[0] : 0; }
+  __device__ __forceinline__ int ncs_of(int q) const { return q ? ncs[1] : ncs[0]; }
+  __device__ __forceinline__ int nrun_of(int q) const { return q ? nrun[1] : nrun[0]; }
+  __device__ __forceinline__ int cs0(int rr) const {
+    return rr < rows[0] ? rr * ncs[0] : rows[0] * ncs[0] + (rr - rows[0]) * ncs[1];
+  }
+  __device__ __forceinline__ int run0(int rr) const {
+    return rr < rows[0] ? rr * nrun[0] : rows[0] * nrun[0] + (rr - rows[0]) * nrun[1];
+  }
+};
+
+// Segment of target (cx, cy) in stencil row oy = s - 1: window positions of the
+// cell boundaries L | C | R | end, and the window row.
+struct Seg {
+  int pL, pC, pR, pE, r;
+};
+template <int BT>
+__device__ __forceinline__ Seg seg_of(const W2Smem<BT>& S, const Geo& G, int b, int cx, int cy,
+                                      int s) {
+  Seg g;
+  g.r = G.row0(b) + (cy + s - S.bx[b][2]);  // window row (ymin-1 is the band's row 0)
+  const short* cs = S.cs + G.cs0(g.r) + (cx - S.bx[b][0]);
+  const int base = S.rbase[g.r];
+  g.pL = base + cs[0];
+  g.pC = base + cs[1];
+  g.pR = base + cs[2];
+  g.pE = base + cs[3];
+  return g;
+}
+
+// Cell blocks [0, ncb): one cell v per thread (see the file comment; first in
+// the grid: their merge is the longest dependency chain). Record blocks
+// [ncb, ...): kPackR records per thread (strided by the block size). The
+// block's cells and their x-neighbours are one CSR span, staged in shared
+// memory. Triples whose span exceeds 32 or that need a wrapped cell get no run
+// list (the sweep takes those rows on the exact path).
+__global__ void __launch_bounds__(256) k_w2_pack(Win2Args a, int ncb) {
+  const int tid = threadIdx.x;
+  if ((int)blockIdx.x < ncb) {
+    constexpr int kSpan = 2048;
+    __shared__ int sid[kSpan];
+    __shared__ int sst[256 + 3];
+    const int64_t C = (int64_t)a.g.counts[0] * a.g.counts[1];
+    const int64_t v0 = (int64_t)blockIdx.x * 256;
+    for (int e = tid; e < 256 + 3; e += 256)
+      sst[e] = __ldg(a.start + min(max(v0 - 1 + e, (int64_t)0), C));
+    __syncthreads();
+    const int lo = sst[0], hi = sst[256 + 2];
+    const bool staged = hi - lo <= kSpan;
+    if (staged)
+      for (int e = tid; e < hi - lo; e += 256) sid[e] = __ldg(a.items + lo + e);
+    __syncthreads();
+    const int* ids = staged ? sid - lo : a.items;
+    const int64_t v = v0 + tid;
+    const int nx = a.g.counts[0];
+    const int x = (int)(v % nx);
+    if (v < C) {
+      const int m1 = sst[tid + 1], m2 = sst[tid + 2];
+      const __half hx = __int2half_rn(x);
+      for (int s = m1; s < m2; ++s) a.wu[s] = hx;
+      const int s0 = x > 0 ? sst[tid] : m1;
+      const int e = x + 1 < nx ? sst[tid + 3] : m2;
+      if (e - s0 <= kSegMax && !(a.g.wrap[0] && (x == 0 || x == nx - 1))) {
+        int iL = s0, iC = m1, iR = m2;
+        int vL = iL < m1 ? ids[iL] : INT_MAX;
+        int vC = iC < m2 ? ids[iC] : INT_MAX;
+        int vR = iR < e ? ids[iR] : INT_MAX;
+        unsigned w[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) w[q] = 0xFFFFFFFFu;
+#pragma unroll
+        for (int t = 0; t < kSegMax; ++t) {
+          if (t >= e - s0) break;
+          const int mn = min(vL, min(vC, vR));
+          const bool tl = mn == vL, tc = !tl && mn == vC;
+          const int pos = tl ? iL : (tc ? iC : iR);
+          if (tl) ++iL;
+          else if (tc) ++iC;
+          else ++iR;
+          const int nxt = pos + 1;
+          const int nv = (tl ? nxt < m1 : (tc ? nxt < m2 : nxt < e)) ? ids[nxt] : INT_MAX;
+          vL = tl ? nv : vL;
+          vC = tc ? nv : vC;
+          vR = (!tl && !tc) ? nv : vR;
+          const unsigned sh = 8 * (t & 3);
+          w[t >> 2] = (w[t >> 2] & ~(0xFFu << sh)) | ((unsigned)(pos - s0) << sh);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(a.wrun + v * kSegMax);
+        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+      }
+    }
+    pdl_trigger();
+    return;
+  }
+  int id[kPackR];
+  double rx[kPackR], ry[kPackR];
+  const int s0 = (blockIdx.x - ncb) * 256 * kPackR + tid;
+#pragma unroll
+  for (int q = 0; q < kPackR; ++q) {
+    const int s = s0 + 256 * q;
+    id[q] = s < a.n ? __ldg(a.items + s) : 0;
+  }
+#pragma unroll
+  for (int q = 0; q < kPackR; ++q) {
+    rx[q] = __ldg(a.rel[0] + id[q]);
+    ry[q] = __ldg(a.rel[1] + id[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < kPackR; ++q) {
+    const int s = s0 + 256 * q;
+    if (s >= a.n) break;
+    const int p = s >> 1, h = s & 1;
+    a.wxy[4 * p + h] = __double2half(rx[q]);
+    a.wxy[4 * p + 2 + h] = __double2half(ry[q]);
+    a.wid[s] = id[q];
+  }
+  pdl_trigger();
+}
+
+__device__ __forceinline__ __half w2_x(const Win2Args& a, int64_t s) {
+  return a.wxy[4 * (s >> 1) + (s & 1)];
+}
+__device__ __forceinline__ __half w2_y(const Win2Args& a, int64_t s) {
+  return a.wxy[4 * (s >> 1) + 2 + (s & 1)];
+}
+
+// The exact per-row path (any input): the reference's 9-cell walk
+// (nnps.cpp:354-410) with its minimum-image offsets dc = -off (:359-362).
+// EMIT: the row is written to dst[0, k) and sorted.
+template <bool EMIT, class Row>
+__device__ int w2_slow_row(const Win2Args& a, int i, int cxi, int cyi, __half rx, __half ry,
+                           const Row& dst) {
+  const int nx = a.g.counts[0], ny = a.g.counts[1];
+  const __half hhx = hb(a.c.h_hh[0]), hhy = hb(a.c.h_hh[1]);
+  const __half thr = hb(a.c.h_thr);
+  int k = 0;
+  for (int oy = -1; oy <= 1; ++oy) {
+    int cy = cyi + oy;
+    if (cy < 0 || cy >= ny) {
+      if (!a.g.wrap[1] || cy < -ny || cy >= 2 * ny) continue;
+      cy = (cy + ny) % ny;
+    }
+    const __half ccy = cc_half(a.c.h_cc[1], oy);
+    for (int ox = -1; ox <= 1; ++ox) {
+      int cx = cxi + ox;
+      if (cx < 0 || cx >= nx) {
+        if (!a.g.wrap[0] || cx < -nx || cx >= 2 * nx) continue;
+        cx = (cx + nx) % nx;
+      }
+      const int64_t c = (int64_t)cy * nx + cx;
+      const int b = __ldg(a.start + c), e = __ldg(a.start + c + 1);
+      const __half ccx = cc_half(a.c.h_cc[0], ox);  // r16(dc*hc), dc = -ox
+      for (int s = b; s < e; ++s) {
+        const int j = __ldg(a.wid + s);
+        if (j == i) continue;
+        const __half dx = __hadd_rn(__hmul_rn(__hsub_rn(rx, w2_x(a, s)), hhx), ccx);
+        const __half dy = __hadd_rn(__hmul_rn(__hsub_rn(ry, w2_y(a, s)), hhy), ccy);
+        const __half acc = __hadd_rn(__hmul_rn(dx, dx), __hmul_rn(dy, dy));
+        if (__hlt(acc, thr)) {
+          if (EMIT) dst.st(k, j);
+          ++k;
+        }
+      }
+    }
+  }
+  if (EMIT) insertion_sort(dst, k);
+  return k;
+}
+
+template <int BT>
+__global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
+  using Cfg = W2Cfg<BT>;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  W2Smem<BT>& S = *reinterpret_cast<W2Smem<BT>*>(smraw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tile = blockIdx.x;  // tiles are dispatched in blockIdx order (look-back)
+  const int r = tile * BT + tid;
+  const bool valid = r < a.nrows;
+  const int i = a.row0 + (valid ? r : 0);
+  const int nx = a.g.counts[0], ny = a.g.counts[1];
+  const uint32_t bar = smem_u32(&S.bar);
+
+  // ---- targets (inputs only: overlaps the pack's tail) ----
+  const int cx = __ldg(a.cellk[0] + i), cy = __ldg(a.cellk[1] + i);
+  const __half rxh = __double2half(__ldg(a.rel[0] + i));
+  const __half ryh = __double2half(__ldg(a.rel[1] + i));
+
+  // ---- bands: split the tile where consecutive targets jump > 2 cells ----
+  if (lane == 31) {
+    S.last[warp][0] = cx;
+    S.last[warp][1] = cy;
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    S.split = BT;
+    S.total = 0;
+    S.bx[0][0] = S.bx[1][0] = INT_MAX;
+    S.bx[0][1] = S.bx[1][1] = INT_MIN;
+    S.bx[0][2] = S.bx[1][2] = INT_MAX;
+    S.bx[0][3] = S.bx[1][3] = INT_MIN;
+  }
+  __syncthreads();
+  int pcx = __shfl_up_sync(0xffffffffu, cx, 1), pcy = __shfl_up_sync(0xffffffffu, cy, 1);
+  if (lane == 0 && warp > 0) {
+    pcx = S.last[warp - 1][0];
+    pcy = S.last[warp - 1][1];
+  }
+  const bool brk = valid && tid > 0 && (abs(cx - pcx) > 2 || abs(cy - pcy) > 2);
+  if (brk) S.split = tid;  // read only when there is exactly one break
+  const int nbrk = __syncthreads_count(brk);
+  bool fast = nbrk <= 1;
+  const int b = (nbrk == 1 && tid >= S.split) ? 1 : 0;
+  if (fast) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const bool in = valid && b == q;
+      const int x0 = __reduce_min_sync(0xffffffffu, in ? cx : INT_MAX);
+      const int x1 = __reduce_max_sync(0xffffffffu, in ? cx : INT_MIN);
+      const int y0 = __reduce_min_sync(0xffffffffu, in ? cy : INT_MAX);
+      const int y1 = __reduce_max_sync(0xffffffffu, in ? cy : INT_MIN);
+      if (lane == 0 && x0 != INT_MAX) {
+        atomicMin(&S.bx[q][0], x0);
+        atomicMax(&S.bx[q][1], x1);
+        atomicMin(&S.bx[q][2], y0);
+        atomicMax(&S.bx[q][3], y1);
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- window geometry (uniform) ----
+  Geo G{};
+  if (fast) {
+    const int nb = nbrk + 1;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const bool on = q < nb;
+      G.rows[q] = on ? S.bx[q][3] - S.bx[q][2] + 3 : 0;
+      G.ncs[q] = on ? S.bx[q][1] - S.bx[q][0] + 4 : 0;
+      G.nrun[q] = on ? S.bx[q][1] - S.bx[q][0] + 1 : 0;
+      if (on) {
+        // rows/cells of the band inside the grid; columns xmin-1 .. xmax+1 must
+        // not wrap a periodic x axis
+        if (S.bx[q][0] < 0 || S.bx[q][1] >= nx || S.bx[q][2] < 0 || S.bx[q][3] >= ny) fast = false;
+        if (a.g.wrap[0] && (S.bx[q][0] == 0 || S.bx[q][1] == nx - 1)) fast = false;
+        if (G.rows[q] > kBandRows) fast = false;
+      }
+    }
+    if (G.cs0(G.rows[0] + G.rows[1]) > Cfg::CSCap || G.run0(G.rows[0] + G.rows[1]) > Cfg::RunCap)
+      fast = false;
+  }
+
+  // ---- window rows (cell_start is an input): a warp per row ----
+  const int nrw = G.rows[0] + G.rows[1];
+  if (fast) {
+    for (int rr = warp; rr < nrw; rr += BT / 32) {
+      const int q = rr < G.rows[0] ? 0 : 1;
+      const int y = S.bx[q][2] - 1 + (rr - G.row0(q));
+      int gy = y;
+      if (y < 0 || y >= ny) gy = a.g.wrap[1] ? (y + ny) % ny : -1;
+      const int ncs = G.ncs_of(q), cs0 = G.cs0(rr);
+      if (gy < 0) {
+        for (int e = lane; e < ncs; e += 32) S.cs[cs0 + e] = 0;
+        if (lane == 0) {
+          S.ra8[rr] = -1;
+          S.rn[rr] = 0;
+          S.rgy[rr] = -1;
+        }
+        continue;
+      }
+      const int64_t row = (int64_t)gy * nx;
+      const int xl = max(S.bx[q][0] - 1, 0), xh = min(S.bx[q][1] + 1, nx - 1);
+      const int s0 = __ldg(a.start + row + xl), s1 = __ldg(a.start + row + xh + 1);
+      const int a8 = s0 & ~7;
+      for (int e = lane; e < ncs; e += 32)
+        S.cs[cs0 + e] = (short)(__ldg(a.start + row + min(max(S.bx[q][0] - 1 + e, 0), nx)) - a8);
+      if (lane == 0) {
+        const int nrec = s1 > s0 ? ((s1 + 7) & ~7) - a8 : 0;
+        S.ra8[rr] = a8;
+        S.rn[rr] = nrec;
+        S.rgy[rr] = gy;
+        atomicAdd(&S.total, nrec);
+      }
+    }
+  }
+  __syncthreads();
+  fast = fast && S.total <= Cfg::WCap;
+
+  // ---- stage the window: TMA bulk copies, one mbarrier ----
+  if (fast && warp == 0) {
+    const int nr = lane < nrw ? S.rn[lane] : 0;
+    int incl = nr;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane < nrw) S.rbase[lane] = incl - nr;
+    __syncwarp();
+    if (lane == 0) {
+      pdl_wait();  // the pack's arrays are complete
+      unsigned tx = (unsigned)S.total * 10u;
+      for (int rr = 0; rr < nrw; ++rr)
+        if (S.rgy[rr] >= 0) tx += 32u * (unsigned)G.nrun_of(rr < G.rows[0] ? 0 : 1);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx)
+                   : "memory");
+      for (int rr = 0; rr < nrw; ++rr) {
+        const int gy = S.rgy[rr];
+        if (gy < 0) continue;
+        const int q = rr < G.rows[0] ? 0 : 1;
+        const int n8 = S.rn[rr], a8 = S.ra8[rr], wb = S.rbase[rr];
+        const void* src[4] = {a.wxy + 2 * (int64_t)a8, a.wu + a8, a.wid + a8,
+                              a.wrun + ((int64_t)gy * nx + S.bx[q][0]) * kSegMax};
+        const uint32_t dst[4] = {smem_u32(&S.c.xy[wb >> 1]), smem_u32(&S.c.u[wb]),
+                                 smem_u32(&S.id[wb]), smem_u32(&S.run[2 * G.run0(rr)])};
+        const unsigned bytes[4] = {4u * n8, 2u * n8, 4u * n8, 32u * (unsigned)G.nrun_of(q)};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (bytes[c] == 0) continue;
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  dst[c]),
+              "l"(src[c]), "r"(bytes[c]), "r"(bar)
+              : "memory");
+        }
+      }
+    }
+  }
+  if (fast) {
+    // one warp polls the barrier; the others wait at __syncthreads (no issue slots)
+    if (warp == 0)
+      asm volatile(
+          "{\n\t.reg .pred P;\n"
+          "W2WAIT:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n\t"
+          "@!P bra W2WAIT;\n\t}" ::"r"(bar)
+          : "memory");
+    __syncthreads();
+  }
+  pdl_wait();  // (the exact path reads the pack's arrays from global memory)
+
+  // ---- A: hit words, row length ----
+  const __half2 hhx = __half2half2(hb(a.c.h_hh[0])), hhy = __half2half2(hb(a.c.h_hh[1]));
+  const __half2 hc2 = __half2half2(hb(a.c.h_cc[0])), thr2 = __half2half2(hb(a.c.h_thr));
+  const __half2 rx2 = __half2half2(rxh), ry2 = __half2half2(ryh);
+  const __half2 ut2 = __half2half2(__int2half_rn(cx));
+  bool slow = !fast || !valid;
+  int k = 0;
+  if (fast) {  // CTA-uniform: every lane runs the warp-uniform loops below
+    int tot = 0;
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      Seg g{0, 0, 0, 0, 0};
+      if (valid) g = seg_of(S, G, b, cx, cy, s);
+      const int p0 = g.pL & ~1;
+      if (g.pE - p0 > kSegMax) slow = true;
+      // pairs of this lane; the loop runs the warp's maximum (lanes past their
+      // segment test the records that follow it, masked out below)
+      const int np = slow ? 0 : (g.pE - p0 + 1) >> 1;
+      const int npmax = __reduce_max_sync(0xffffffffu, np);
+      const __half2 ccy = __half2half2(cc_half(a.c.h_cc[1], s - 1));
+      const uint2* xyp = S.c.xy + (p0 >> 1);
+      const unsigned* up = reinterpret_cast<const unsigned*>(S.c.u + p0);
+      unsigned H = 0;
+      // groups of 4 pairs with no branch between them, so the 4 dependent
+      // binary16 chains interleave
+#pragma unroll
+      for (int t0 = 0; t0 < kSegMax / 2; t0 += 4) {
+        if (t0 >= npmax) break;
+        uint2 xy[4];
+        unsigned u2[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          xy[t] = xyp[t0 + t];
+          u2[t] = up[t0 + t];
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          pair_test(xy[t].x, xy[t].y, u2[t], rx2, ry2, ut2, hhx, hhy, hc2, ccy, s != 1, thr2,
+                    1u << (2 * (t0 + t)), H);
+      }
+      H &= above(g.pL - p0) & ~above(g.pE - p0);  // bit q = position p0 + q
+      if (s == 1 && !slow) {
+        // the target's own record: its id among the (ascending) ids of its cell
+        int lo = g.pC, hi = g.pR;
+        while (lo < hi) {
+          const int m = (lo + hi) >> 1;
+          if (S.id[m] < i) lo = m + 1;
+          else hi = m;
+        }
+        if (lo < g.pR && S.id[lo] == i) H &= ~(1u << (lo - p0));
+        else slow = true;  // RelCoords cell is not the CSR cell (a stale grid)
+      }
+      S.hw[s][tid] = H;
+      tot += __popc(H);
+    }
+    k = tot;
+  }
+  if (valid && slow) k = w2_slow_row<false>(a, i, cx, cy, rxh, ryh, GlobalRow{nullptr});
+
+  // ---- block scan, publish ----
+  const int incl = warp_inclusive_scan(k);
+  if (lane == 31) S.wsum[warp] = incl;
+  __syncthreads();
+  int wbase = 0, btot = 0;
+#pragma unroll
+  for (int u = 0; u < BT / 32; ++u) {
+    wbase += u < warp ? S.wsum[u] : 0;
+    btot += S.wsum[u];
+  }
+  const int excl = wbase + incl - k;
+  if (tid == 0) lb_publish(a.tiles, tile, btot, a.epoch);
+
+  // ---- B: sorted rows ----
+  // The run list of the target's centre cell walks each segment in id order, so
+  // hits are appended sorted: a warp-uniform walk, four positions per step.
+  auto build = [&](const auto& dst, bool part) {
+    int kk = 0;
+#pragma unroll 1
+    for (int s = 0; s < 3; ++s) {
+      const unsigned H = part ? S.hw[s][tid] : 0u;
+      Seg g{0, 0, 0, 0, 0};
+      if (H) g = seg_of(S, G, b, cx, cy, s);
+      const int pL = g.pL, len = g.pE - g.pL;
+      const int lmax = __reduce_max_sync(0xffffffffu, len);
+      if (lmax == 0) continue;
+      const unsigned hrel = H >> (pL & 1);  // bit o = position pL + o
+      const uint4* rl = &S.run[2 * (H ? G.run0(g.r) + cx - S.bx[b][0] : 0)];
+      uint4 w[2];
+      w[0] = rl[0];
+      w[1] = rl[1];
+      const int gs = kk;
+      const uint32_t idb = smem_u32(S.id) + 4u * (uint32_t)pL;
+#pragma unroll
+      for (int t4 = 0; t4 < 8; ++t4) {
+        if (4 * t4 >= lmax) break;
+        const unsigned word = t4 < 4 ? (&w[0].x)[t4] : (&w[1].x)[t4 - 4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const unsigned off = (word >> (8 * u)) & 0xFFu;  // 0xFF past the run
+          unsigned sh;
+          asm("shr.b32 %0, %1, %2;" : "=r"(sh) : "r"(hrel), "r"(off));  // (0 for off >= 32)
+          const bool hit = sh & 1u;
+          if (hit) {
+            int v;
+            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(idb + 4u * off));
+            dst.st(kk, v);
+          }
+          kk += hit;
+        }
+      }
+      if (gs > 0 && kk > gs && dst.ld(gs) < dst.ld(gs - 1)) merge_tail(dst, gs, kk);
+    }
+  };
+  const bool fits = btot <= Cfg::PCap;
+  if (fits) {
+    const SharedRow row{smem_u32(S.pk) + 4u * (uint32_t)excl};
+    if (fast) build(row, valid && !slow);
+    if (valid && slow && k > 0) w2_slow_row<true>(a, i, cx, cy, rxh, ryh, row);
+  }
+
+  if (warp == 0) {
+    const long long bse = lb_resolve(a.tiles, tile, btot, a.epoch);
+    if (lane == 0) S.base = bse;
+  }
+  __syncthreads();
+  const long long base = S.base;
+  if (valid) a.offsets[r] = base + excl;
+  if (r == a.nrows - 1) a.offsets[a.nrows] = base + excl + k;
+  if (base + btot > a.capacity) return;
+  int32_t* gout = a.out + base;
+  if (!fits) {
+    const GlobalRow row{gout + excl};
+    if (fast) build(row, valid && !slow);
+    if (valid && slow && k > 0) w2_slow_row<true>(a, i, cx, cy, rxh, ryh, row);
+    return;
+  }
+  stream_tile<BT>(gout, SharedRow{smem_u32(S.pk)}, btot, tid);
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+// rows per tile: SPHX_W2BT=128|256 (default 128)
+int w2_bt() {
+  static int bt = 0;
+  if (!bt) {
+    const char* e = std::getenv("SPHX_W2BT");
+    bt = (e && std::atoi(e) == 256) ? 256 : 128;
+  }
+  return bt;
+}
+
+template <int BT>
+void launch_sweep_bt(const Win2Args& a, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_w2<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(W2Smem<BT>));
+    attr = true;
+  }
+  launch_pdl(k_w2<BT>, (unsigned)((a.nrows + BT - 1) / BT), BT, sizeof(W2Smem<BT>), st, a);
+}
+
+}  // namespace
+
+int64_t win2_tiles(int64_t nrows) { return (nrows + w2_bt() - 1) / w2_bt(); }
+
+// pack + sweep; returns the number of kernels launched
+int launch_win2(const Win2Args& a, cudaStream_t st) {
+  const int nbr = (a.n + 256 * kPackR - 1) / (256 * kPackR);
+  const int64_t C = (int64_t)a.g.counts[0] * a.g.counts[1];
+  const int ncb = (int)((C + 255) / 256);
+  k_w2_pack<<<(unsigned)(ncb + nbr), 256, 0, st>>>(a, ncb);
+  if (w2_bt() == 256) launch_sweep_bt<256>(a, st);
+  else launch_sweep_bt<128>(a, st);
+  return 2;
+}
+
+}  // namespace sphx_dev
