@@ -4,9 +4,11 @@ BASELINE config C2 (2-D jittered lattice 1000x1000 = 1M particles).
 
 A *step* is one drop-in ``rcll(rel, grid, fp16)`` call on device-resident inputs
 (RelCoords + CellGrid CSR in HBM) producing the contract-exact CSR neighbour table
-in HBM: encode kernel + fused sweep kernel. ``e2e`` is the same call through the
-C ABI with pinned host buffers (H2D of the inputs and D2H of the whole table
-inside the timed region). ``--impl reference`` times the reference's own CPU
+in HBM (2-D FP16: the pack + windowed sweep kernels, window.cu). ``e2e`` is the
+same call through the C ABI (sphx_rcll + sphx_table_copy) with pinned host
+buffers; ``e2e.dropin`` is the reference's own C++ API, ``sphx::rcll`` via
+``_core`` (host std::vectors in, owning NeighborTable out). Both put the H2D of
+the inputs and the D2H of the whole table inside the timed region. ``--impl reference`` times the reference's own CPU
 implementation (oracle/_ref, all host threads) on the same workload.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
@@ -119,14 +121,22 @@ def golden(config, precision):
 
 
 def ncu_traffic(config, precision):
-    """Per-launch DRAM bytes of the sweep kernel from the committed ncu capture."""
-    p = os.path.join(ROOT, "profiles", "ncu_sweep_summary.json")
+    """Per-step memory traffic of the step's kernels from the ncu capture committed
+    with the code (profiles/r2_traffic.json, tools/traffic.sh): DRAM bytes read and
+    written with a cold L2 (ncu flushes caches before each kernel), and the bytes the
+    kernels write into L2 (every write leaves the SM; the DRAM write counter misses
+    what is still dirty in the 126 MB L2 when the kernel ends)."""
+    p = os.path.join(ROOT, "profiles", "r2_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
-    e = d.get(f"{config}_{precision}")
-    return None if e is None else e.get("dram_bytes")
+    e = d.get("configs", {}).get(f"{config}_{precision}")
+    if e is None:
+        return None
+    return {"read": e["dram_read"], "write": e["l2_write"], "dram_write": e["dram_write"],
+            "kernels": e.get("kernels"), "source": "profiles/r2_traffic.json",
+            "commit": d.get("commit")}
 
 
 # ---------------------------------------------------------------------------------------
@@ -185,6 +195,12 @@ class ClockSampler:
 # ---------------------------------------------------------------------------------------
 # distributed plumbing (one process per GPU; N>1 via torchrun)
 # ---------------------------------------------------------------------------------------
+def config_dict(args, w, n):
+    """The workload, identical in both arms' JSON lines."""
+    return {"workload": w["desc"], "n_particles": n, "precision": args.precision,
+            "backend": "rcll", "order": getattr(args, "order", "lattice")}
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -234,8 +250,7 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": w["desc"], "n_particles": n, "precision": args.precision,
-                       "backend": "rcll"},
+            "config": config_dict(args, w, n),
             "cpu_baseline": {"value": v, "unit": "particles/s", "cores": threads, "kind": kind,
                              "sample": f"full {args.config} per step, rcll() only (grid and "
                                        "RelCoords built outside the timer, experiments.cpp:"
@@ -445,6 +460,8 @@ def run_ours(args):
     if args.op == "step":
         return bench_step(args, w, ctx, stream, grid, n, C, xd, rel, cell, cell_of, items, start,
                           local)
+    # host positions for the drop-in e2e (sphx::rcll through _core)
+    x_host = None if w.get("device_lattice") else [t.cpu().numpy() for t in xd]
     del xd
     offsets = torch.empty(n + 1, dtype=torch.int64, device=dev)
     cap = n * (24 if dim == 2 else 60)
@@ -524,6 +541,29 @@ def run_ours(args):
                 e2e_t.append(time.perf_counter() - t0)
             assert tot == total
 
+        # ---- e2e at the real drop-in: sphx::rcll (nnps.hpp:41) through `_core`, the
+        # reference's own C++ API: host RelCoords/CellGrid in, an owning NeighborTable
+        # (std::vector, pageable) out; grid + RelCoords built outside the timer like
+        # exp_scaling (experiments.cpp:268-300)
+        api_t, api_hash = [], None
+        if e2e_ok and x_host is not None:
+            from paper_2401_08586_b200 import _core as core
+            ps = core.ParticleSystem(core.Domain.unit(dim), ds, n)
+            for k in range(dim):
+                ps.set_x(k, x_host[k])
+            cg = core.make_grid_for(ps)
+            cg.rebin(ps)
+            rc = core.build_rel_coords(ps, cg)
+            cprec = [core.Precision.fp64, core.Precision.fp32, core.Precision.fp16][prec]
+            for _ in range(2):
+                tab = core.rcll(rc, cg, cprec)
+            for _ in range(args.e2e_steps):
+                t0 = time.perf_counter()
+                tab = core.rcll(rc, cg, cprec)
+                api_t.append(time.perf_counter() - t0)
+            api_hash = P.capi.table_hash(tab.offsets(), tab.items())
+            del tab, rc, cg, ps
+
     # ---- parity of the timed output -------------------------------------------------------
     if reorder is not None:  # the golden lattice-order table, renumbered
         perm, g_off, g_it, g_ok = reorder
@@ -540,8 +580,10 @@ def run_ours(args):
         e2e_hash = P.capi.table_hash(h_off.numpy(), h_out.numpy()) if h_out is not None else dev_hash
         parity = {"bit_exact_vs_reference_hash": (total == gold["total"]
                                                   and f"{dev_hash:016x}" == gold["hash"]
-                                                  and e2e_hash == dev_hash),
-                  "hash": f"{dev_hash:016x}", "golden": gold["hash"]}
+                                                  and e2e_hash == dev_hash
+                                                  and api_hash in (None, dev_hash)),
+                  "hash": f"{dev_hash:016x}", "golden": gold["hash"],
+                  "e2e_tables": "C-ABI and sphx::rcll tables hash-equal to the timed table"}
     else:  # too large for a full reference table: sampled rows
         parity = sampled_parity(args.config, w, grid, prec, rel, cell, start, items, offsets, out,
                                 total)
@@ -549,11 +591,13 @@ def run_ours(args):
     t_step = statistics.median(step_ms) * 1e-3
     t_sweep = statistics.median(sweep_ms) * 1e-3
     t_e2e = statistics.median(e2e_t) if e2e_t else None
+    t_api = statistics.median(api_t) if api_t else None
     s_pos = {0: 8, 1: 4, 2: 2}[prec] * dim
     b_sweep = n * s_pos + 4 * n + 4 * (C + 1) + 8 * (n + 1) + 4 * total
     b_pipe = b_sweep + 8 * dim * n + 4 * dim * n + 4 * n + n * (s_pos + 4)
     peak, peak_kind = measured_peaks()
     achieved = b_sweep / t_sweep / 1e9
+    traffic = ncu_traffic(args.config, args.precision)
     h2d = (dim * n * 12 + 4 * n + 4 * (C + 1)) if e2e_t else 0
     d2h = ((n + 1) * 8 + total * 4 + 8) if e2e_t else 0
     line = {
@@ -564,22 +608,27 @@ def run_ours(args):
         "vs_baseline_basis": "BASELINE.md: paper Table 6 FP16 RCLL 1M sorted on A100, 2.60 ms",
         "dtype": "f16" if prec == 2 else ("f32" if prec == 1 else "f64"),
         "data": "synthetic (reference build_lattice generator, seed 1)",
-        "config": {"workload": w["desc"], "n_particles": n, "cells": C, "pairs": total,
-                   "precision": args.precision, "backend": "rcll",
-                   "input": "device-resident RelCoords (fp64) + CellGrid CSR",
-                   "order": args.order,
-                   "l2": "flushed between timed steps (256 MiB write, outside the events)"},
+        "config": config_dict(args, w, n),
+        "setup": {"cells": C, "pairs": total,
+                  "input": "device-resident RelCoords (fp64) + CellGrid CSR",
+                  "l2": "flushed between timed steps (256 MiB write, outside the events)"},
         "parity": parity,
         "breakdown_ms": {"encode": statistics.median(encode_ms), "sweep": t_sweep * 1e3,
                          "step": t_step * 1e3, "wall_per_step": t_wall / args.steps * 1e3},
         "roofline": {"bound": "hbm",
-                     "kernel": ("k_rcll16 (single pass: tests, sorted rows, tile look-back, "
-                                "16-byte stores)") if (dim == 2 and prec == 2) else
+                     "kernel": ("k_w2_pack + k_w2 (CSR-order binary16 pack and run lists; "
+                                "windows staged by TMA bulk copies, pair tests from shared "
+                                "memory, sorted rows from the run lists, tile look-back)")
+                               if (dim == 2 and prec == 2 and os.environ.get("SPHX_W2") != "0")
+                               else ("k_encode_rows + k_rcll16") if (dim == 2 and prec == 2) else
                                ("k_r16_test + k_r16_emit" if (dim == 3 and prec == 2) else
                                 "k_sweep (single pass)"),
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": ncu_traffic(args.config, args.precision),
+                     "traffic": traffic["read"] + traffic["write"] if traffic else None,
+                     "traffic_read": traffic["read"] if traffic else None,
+                     "traffic_write": traffic["write"] if traffic else None,
+                     "traffic_detail": traffic,
                      "algorithmic_bytes": b_sweep,
                      "bytes_formula": "N*S_pos + 4N + 4(C+1) + 8(N+1) + 4P",
                      "pipeline": {"bytes": b_pipe, "achieved": b_pipe / t_step / 1e9,
@@ -588,7 +637,13 @@ def run_ours(args):
                                              "+ 4N (items) + N*(S_pos+4) (encoded records)"}},
         "e2e": ({"value": n / t_e2e, "unit": "particles/s", "ms_per_step": t_e2e * 1e3,
                  "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                 "api": "sphx_rcll + sphx_table_copy (C ABI), pinned host buffers"} if e2e_t else
+                 "api": "sphx_rcll + sphx_table_copy (the C ABI the reference's FFI binds, "
+                        "include/sphx_cuda.h), pinned host buffers",
+                 "dropin": ({"value": n / t_api, "ms_per_step": t_api * 1e3,
+                             "api": "sphx::rcll(RelCoords, CellGrid, Precision) (nnps.hpp:41) "
+                                    "through the pybind11 module _core: host std::vector "
+                                    "inputs, owning NeighborTable out (its 78 MB first touch "
+                                    "included)"} if t_api else None)} if e2e_t else
                 {"value": None, "unit": "particles/s", "h2d_bytes_per_step": 0,
                  "d2h_bytes_per_step": 0,
                  "reason": f"table of {total * 4 / 2**30:.1f} GiB exceeds the 8 GiB pinned-host budget"}),

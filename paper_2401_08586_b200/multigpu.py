@@ -247,7 +247,20 @@ def agree_capacity(state: SlabState, group=None) -> int:
     return int(t.item())
 
 
+def _nvtx(name):
+    """NVTX range (Nsight) around a host-side phase; a no-op without CUDA."""
+    import contextlib
+    if torch.cuda.is_available():
+        return torch.cuda.nvtx.range(name)
+    return contextlib.nullcontext()
+
+
 def exchange_nccl(st: SlabState, group=None):
+    with _nvtx("sphx.halo"):
+        _exchange_nccl(st, group)
+
+
+def _exchange_nccl(st: SlabState, group=None):
     """First layer -> prev, last layer -> next, halos <- both, in one NCCL group.
     Operations are posted in the same order on every rank, so NCCL's in-order
     matching of point-to-point pairs is right even when prev == next (world 2,
@@ -270,6 +283,11 @@ def exchange_nccl(st: SlabState, group=None):
 
 
 def exchange_gloo(st: SlabState, group=None):
+    with _nvtx("sphx.halo"):
+        _exchange_gloo(st, group)
+
+
+def _exchange_gloo(st: SlabState, group=None):
     """The same exchange staged through host memory over gloo (ranks sharing a
     GPU, where NCCL cannot run): device -> host, tagged send/recv, host -> device."""
     prv, nxt = st.plan.prev(st.rank), st.plan.next(st.rank)
