@@ -11,7 +11,7 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
     --log-file gpurun_out/launches_${TAG}.csv \
     python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 "$@" > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_(rcll16|r16_test|r16_emit|encode_rows|encode_xy)" -s 6 -c 3 \
+    -k regex:"k_(w2|rcll16|r16_test|r16_emit|encode_rows|encode_xy)" -s 6 -c 3 \
     -o gpurun_out/prof_${TAG} \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 "$@" \
     > gpurun_out/ncu_${TAG}.log 2>&1
