@@ -36,9 +36,10 @@
 //                  in shared memory (over the dead coordinates), 16-byte stores.
 //
 // Tiles whose targets do not form <= 2 compact bands (a shuffled particle order),
-// whose window exceeds shared memory or wraps a periodic x axis, and targets whose
-// segment exceeds 32 positions or whose RelCoords cell is not their CSR cell take
-// an exact per-row path that walks the 9 cells in global memory like the
+// whose window exceeds shared memory or wraps a periodic x axis run the same A
+// and B on the pack's CSR-order arrays in global memory. Targets whose segment
+// exceeds 32 positions, wraps a periodic x axis there, or whose RelCoords cell is
+// not their CSR cell take an exact per-row path that walks the 9 cells like the
 // reference (nnps.cpp:354-410) and sorts the row.
 //
 // Exactness (per candidate, nnps.cpp:332-346, nnps_batch.cpp:238-258):
@@ -241,6 +242,27 @@ struct W2Smem {
   unsigned long long bar;
 };
 
+// Where a segment's records are read from: the staged window (shared memory,
+// window positions) or the pack's CSR-order arrays (global memory, CSR
+// positions; tiles without a window). Positions keep their parity in both, so
+// pair p/2 is the same record pair.
+struct SmemSrc {
+  const uint2* xy;
+  const unsigned* u;
+  const int* id;
+  __device__ __forceinline__ uint2 pair(int q) const { return xy[q]; }
+  __device__ __forceinline__ unsigned upair(int q) const { return u[q]; }
+  __device__ __forceinline__ int ident(int p) const { return id[p]; }
+};
+struct GlobSrc {
+  const uint2* xy;
+  const unsigned* u;
+  const int* id;
+  __device__ __forceinline__ uint2 pair(int q) const { return __ldg(xy + q); }
+  __device__ __forceinline__ unsigned upair(int q) const { return __ldg(u + q); }
+  __device__ __forceinline__ int ident(int p) const { return __ldg(id + p); }
+};
+
 // Band geometry (identical in every thread: computed from S.bx).
 struct Geo {
   int rows[2], ncs[2], nrun[2];
@@ -271,6 +293,31 @@ __device__ __forceinline__ Seg seg_of(const W2Smem<BT>& S, const Geo& G, int b, 
   g.pC = base + cs[1];
   g.pR = base + cs[2];
   g.pE = base + cs[3];
+  return g;
+}
+
+// Segment of target (cx, cy) in stencil row oy = s - 1 from the CSR (tiles
+// without a window): CSR positions of the cell boundaries L | C | R | end and
+// the centre cell (its run list). ok = false: the segment wraps a periodic x
+// axis (the exact path); an absent row (walled y) is an empty segment.
+__device__ __forceinline__ Seg seg_glob(const Win2Args& a, int cx, int cy, int s, bool& ok) {
+  Seg g{0, 0, 0, 0, -1};
+  const int nx = a.g.counts[0], ny = a.g.counts[1];
+  if (a.g.wrap[0] && (cx == 0 || cx == nx - 1)) {
+    ok = false;
+    return g;
+  }
+  int y = cy + s - 1;
+  if (y < 0 || y >= ny) {
+    if (!a.g.wrap[1]) return g;
+    y = (y + ny) % ny;
+  }
+  const int64_t row = (int64_t)y * nx;
+  g.pL = __ldg(a.start + row + max(cx - 1, 0));
+  g.pC = __ldg(a.start + row + cx);
+  g.pR = __ldg(a.start + row + cx + 1);
+  g.pE = __ldg(a.start + row + min(cx + 1, nx - 1) + 1);
+  g.r = (int)(row + cx);  // the centre cell
   return g;
 }
 
@@ -592,14 +639,27 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
   const __half2 hc2 = __half2half2(hb(a.c.h_cc[0])), thr2 = __half2half2(hb(a.c.h_thr));
   const __half2 rx2 = __half2half2(rxh), ry2 = __half2half2(ryh);
   const __half2 ut2 = __half2half2(__int2half_rn(cx));
-  bool slow = !fast || !valid;
+  bool slow = !valid;
   int k = 0;
-  if (fast) {  // CTA-uniform: every lane runs the warp-uniform loops below
+  const SmemSrc ssrc{S.c.xy, reinterpret_cast<const unsigned*>(S.c.u), S.id};
+  const GlobSrc gsrc{reinterpret_cast<const uint2*>(a.wxy), reinterpret_cast<const unsigned*>(a.wu),
+                     a.wid};
+  // segment s of this lane's target: window positions (fast tile) or CSR
+  // positions (tile without a window)
+  auto seg = [&](int s) -> Seg {
+    Seg g{0, 0, 0, 0, -1};
+    if (!valid || slow) return g;
+    if (fast) return seg_of(S, G, b, cx, cy, s);
+    bool ok = true;
+    g = seg_glob(a, cx, cy, s, ok);
+    if (!ok) slow = true;
+    return g;
+  };
+  auto phase_a = [&](const auto& src) {  // every lane: warp-uniform loops
     int tot = 0;
 #pragma unroll
     for (int s = 0; s < 3; ++s) {
-      Seg g{0, 0, 0, 0, 0};
-      if (valid) g = seg_of(S, G, b, cx, cy, s);
+      const Seg g = seg(s);
       const int p0 = g.pL & ~1;
       if (g.pE - p0 > kSegMax) slow = true;
       // pairs of this lane; the loop runs the warp's maximum (lanes past their
@@ -607,8 +667,7 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
       const int np = slow ? 0 : (g.pE - p0 + 1) >> 1;
       const int npmax = __reduce_max_sync(0xffffffffu, np);
       const __half2 ccy = __half2half2(cc_half(a.c.h_cc[1], s - 1));
-      const uint2* xyp = S.c.xy + (p0 >> 1);
-      const unsigned* up = reinterpret_cast<const unsigned*>(S.c.u + p0);
+      const int q0 = p0 >> 1;
       unsigned H = 0;
       // groups of 4 pairs with no branch between them, so the 4 dependent
       // binary16 chains interleave
@@ -619,8 +678,8 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
         unsigned u2[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-          xy[t] = xyp[t0 + t];
-          u2[t] = up[t0 + t];
+          xy[t] = src.pair(q0 + t0 + t);
+          u2[t] = src.upair(q0 + t0 + t);
         }
 #pragma unroll
         for (int t = 0; t < 4; ++t)
@@ -633,17 +692,19 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
         int lo = g.pC, hi = g.pR;
         while (lo < hi) {
           const int m = (lo + hi) >> 1;
-          if (S.id[m] < i) lo = m + 1;
+          if (src.ident(m) < i) lo = m + 1;
           else hi = m;
         }
-        if (lo < g.pR && S.id[lo] == i) H &= ~(1u << (lo - p0));
+        if (lo < g.pR && src.ident(lo) == i) H &= ~(1u << (lo - p0));
         else slow = true;  // RelCoords cell is not the CSR cell (a stale grid)
       }
       S.hw[s][tid] = H;
       tot += __popc(H);
     }
     k = tot;
-  }
+  };
+  if (fast) phase_a(ssrc);  // (CTA-uniform)
+  else phase_a(gsrc);
   if (valid && slow) k = w2_slow_row<false>(a, i, cx, cy, rxh, ryh, GlobalRow{nullptr});
 
   // ---- block scan, publish ----
@@ -662,23 +723,28 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
   // ---- B: sorted rows ----
   // The run list of the target's centre cell walks each segment in id order, so
   // hits are appended sorted: a warp-uniform walk, four positions per step.
-  auto build = [&](const auto& dst, bool part) {
+  auto build_src = [&](const auto& dst, bool part, const auto& src) {
     int kk = 0;
 #pragma unroll 1
     for (int s = 0; s < 3; ++s) {
       const unsigned H = part ? S.hw[s][tid] : 0u;
-      Seg g{0, 0, 0, 0, 0};
-      if (H) g = seg_of(S, G, b, cx, cy, s);
+      Seg g{0, 0, 0, 0, -1};
+      if (H) g = seg(s);
       const int pL = g.pL, len = g.pE - g.pL;
       const int lmax = __reduce_max_sync(0xffffffffu, len);
       if (lmax == 0) continue;
       const unsigned hrel = H >> (pL & 1);  // bit o = position pL + o
-      const uint4* rl = &S.run[2 * (H ? G.run0(g.r) + cx - S.bx[b][0] : 0)];
       uint4 w[2];
-      w[0] = rl[0];
-      w[1] = rl[1];
+      if (fast) {
+        const uint4* rl = &S.run[2 * (H ? G.run0(g.r) + cx - S.bx[b][0] : 0)];
+        w[0] = rl[0];
+        w[1] = rl[1];
+      } else {
+        const uint4* rl = reinterpret_cast<const uint4*>(a.wrun) + 2 * (int64_t)(H ? g.r : 0);
+        w[0] = __ldg(rl);
+        w[1] = __ldg(rl + 1);
+      }
       const int gs = kk;
-      const uint32_t idb = smem_u32(S.id) + 4u * (uint32_t)pL;
 #pragma unroll
       for (int t4 = 0; t4 < 8; ++t4) {
         if (4 * t4 >= lmax) break;
@@ -689,21 +755,21 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
           unsigned sh;
           asm("shr.b32 %0, %1, %2;" : "=r"(sh) : "r"(hrel), "r"(off));  // (0 for off >= 32)
           const bool hit = sh & 1u;
-          if (hit) {
-            int v;
-            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(idb + 4u * off));
-            dst.st(kk, v);
-          }
+          if (hit) dst.st(kk, src.ident(pL + (int)off));
           kk += hit;
         }
       }
       if (gs > 0 && kk > gs && dst.ld(gs) < dst.ld(gs - 1)) merge_tail(dst, gs, kk);
     }
   };
+  auto build = [&](const auto& dst, bool part) {
+    if (fast) build_src(dst, part, ssrc);
+    else build_src(dst, part, gsrc);
+  };
   const bool fits = btot <= Cfg::PCap;
   if (fits) {
     const SharedRow row{smem_u32(S.pk) + 4u * (uint32_t)excl};
-    if (fast) build(row, valid && !slow);
+    build(row, valid && !slow);
     if (valid && slow && k > 0) w2_slow_row<true>(a, i, cx, cy, rxh, ryh, row);
   }
 
@@ -719,7 +785,7 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
   int32_t* gout = a.out + base;
   if (!fits) {
     const GlobalRow row{gout + excl};
-    if (fast) build(row, valid && !slow);
+    build(row, valid && !slow);
     if (valid && slow && k > 0) w2_slow_row<true>(a, i, cx, cy, rxh, ryh, row);
     return;
   }
