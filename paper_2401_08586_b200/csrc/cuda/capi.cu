@@ -461,9 +461,14 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
     if (pc.h_thr != 0) {  // (thr == 0: no pair can hit; the generic path handles it)
       // windowed path (window.cu): pack + sweep in run_sweep, no encode
       const size_t np = (size_t)n + 64;
-      TRY(ctx->w_xy.ensure(4 * np));
-      TRY(ctx->w_u.ensure(2 * np));
-      TRY(ctx->w_id.ensure(4 * np));
+      // lanes past their segment read up to 32 records beyond it (masked out):
+      // fresh buffers are zeroed once so that the padding past n is defined
+      for (Buf* b : {&ctx->w_xy, &ctx->w_u, &ctx->w_id}) {
+        const size_t want = (b == &ctx->w_u ? 2 : 4) * np;
+        const void* old = b->p;
+        TRY(b->ensure(want));
+        if (b->p != old) CK(cudaMemsetAsync(b->p, 0, b->bytes, st));
+      }
       TRY(ctx->w_run.ensure(32 * (size_t)C));
       SweepArgs& a = *out;
       a.g = grid_consts(g);

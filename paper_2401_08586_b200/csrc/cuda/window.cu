@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
     pcy = S.last[warp - 1][1];
   }
   const bool brk = valid && tid > 0 && (abs(cx - pcx) > 2 || abs(cy - pcy) > 2);
-  if (brk) S.split = tid;  // read only when there is exactly one break
+  if (brk) atomicMin(&S.split, tid);  // read only when there is exactly one break
   const int nbrk = __syncthreads_count(brk);
   bool fast = nbrk <= 1;
   const int b = (nbrk == 1 && tid >= S.split) ? 1 : 0;
