@@ -53,10 +53,6 @@ int launch_kick_drift(int dim, const StepArgs& a, cudaStream_t st);
 // window.cu
 int64_t win2_tiles(int64_t nrows);
 int launch_win2(const Win2Args& a, cudaStream_t st);
-// tiled.cu
-void tiled2_shape(int nx, int ny, int64_t n, int* tw, int* tpr, int64_t* ntiles);
-int64_t tiled2_scan_tiles(int64_t nrows);
-int launch_tiled2(const TileArgs& a, bool count, cudaStream_t st);
 // slab.cu
 int launch_slab_assemble(const SlabArgs& a, cudaStream_t st);
 }  // namespace sphx_dev
@@ -156,8 +152,6 @@ struct sphx_context {
   Buf b_counts, b_slot, b_bad, b_tiles, b_out_cellof, b_out_start, b_out_items, b_rel[3], b_cell[3];
   // device time step: stress (sigma, tau, eps), rates, displacement, max |dx|, status
   Buf s_stress, s_rates, s_dx, s_flags;
-  // cell-tiled 2-D FP16 RCLL: row lengths, hit words, per-row path flags
-  Buf tl_cnt, tl_mw, tl_mx, tl_flag, tl_rank;
   // windowed 2-D FP16 RCLL: CSR-order binary16 x/y pairs, cell x, ids, run lists
   Buf w_xy, w_u, w_id, w_run;
   // pinned staging for pageable host buffers (two chunks) and their events
@@ -418,13 +412,6 @@ struct RowSel {
   const int32_t* ids = nullptr;
 };
 
-// The cell-tiled 2-D FP16 RCLL path (tiled.cu) is opt-in while it is slower than
-// the encode + k_rcll16 path: SPHX_TILED2=1.
-bool tiled2_enabled() {
-  const char* e = std::getenv("SPHX_TILED2");
-  return e && e[0] == '1';
-}
-
 // The windowed 2-D FP16 RCLL path (window.cu) is the default; SPHX_W2=0 selects
 // the encode + k_rcll16 path.
 bool win2_enabled() {
@@ -435,7 +422,7 @@ bool win2_enabled() {
 int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n64,
                 const double* const src[3], const int32_t* const cellk[3], const int32_t* items,
                 const int32_t* start, const int32_t* cell_of, int prec, double h, int64_t* d_off,
-                SweepArgs* out, const RowSel& sel = RowSel(), bool allow_tiled = true) {
+                SweepArgs* out, const RowSel& sel = RowSel(), bool allow_window = true) {
   if (n64 > INT32_MAX - 64)
     return fail(SPHX_ERR_INVALID_ARGUMENT, "too many particles for one context (int32 ids)");
   const int n = (int)n64;
@@ -455,8 +442,8 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
     return SPHX_OK;
   }
   const int64_t C = mode == MODE_ALL ? 0 : cell_total(g);
-  if (allow_tiled && g.dim == 2 && prec == SPHX_FP16 && mode == MODE_RCLL && !sel.ids &&
-      g.counts[0] <= 2048 && win2_enabled() && !tiled2_enabled()) {
+  if (allow_window && g.dim == 2 && prec == SPHX_FP16 && mode == MODE_RCLL && !sel.ids &&
+      g.counts[0] <= 2048 && win2_enabled()) {
     const PrecConsts pc = make_consts(mode, prec, g, h);
     if (pc.h_thr != 0) {  // (thr == 0: no pair can hit; the generic path handles it)
       // windowed path (window.cu): pack + sweep in run_sweep, no encode
@@ -486,29 +473,6 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
       }
       return SPHX_OK;
     }
-  }
-  if (allow_tiled && g.dim == 2 && prec == SPHX_FP16 && mode == MODE_RCLL && tiled2_enabled()) {
-    // the cell-tiled path (tiled.cu): no encode, count -> scan -> fill in run_sweep
-    TRY(ctx->tl_cnt.ensure(sizeof(int32_t) * (size_t)nrows));
-    TRY(ctx->tl_mw.ensure(sizeof(uint32_t) * 3 * (size_t)n));
-    TRY(ctx->tl_mx.ensure(sizeof(uint32_t) * 3 * (size_t)n));
-    TRY(ctx->tl_flag.ensure((size_t)n));
-    TRY(ctx->tl_rank.ensure(sizeof(uint32_t) * (size_t)n));
-    SweepArgs& a = *out;
-    a.g = grid_consts(g);
-    a.c = make_consts(mode, prec, g, h);
-    a.tiled = 1;
-    for (int k = 0; k < 3; ++k) {
-      a.src[k] = k < g.dim ? src[k] : nullptr;
-      a.cellk[k] = cellk ? cellk[k] : nullptr;
-    }
-    a.start = start;
-    a.cell_of = cell_of;
-    if (ctx->timing) {
-      CK(cudaEventRecord(ctx->ev[0], st));
-      CK(cudaEventRecord(ctx->ev[1], st));
-    }
-    return SPHX_OK;
   }
   const int64_t chunks = chunk_capacity(g.dim, prec, mode, n, C);
   // record indices (selfpos) are 32-bit and chunk starts (xy_cstart) 31-bit
@@ -559,7 +523,6 @@ int run_sweep(sphx_context* ctx, int dim, int prec, int mode, SweepArgs& a, int3
   if (a.n == 0 || a.nrows == 0) return SPHX_OK;
   cudaStream_t st = ctx->stream;
   const int64_t nt = a.win2    ? win2_tiles(a.nrows)
-                     : a.tiled ? tiled2_scan_tiles(a.nrows)
                                : (a.nrows + sweep_tile(dim, prec, mode) - 1) / sweep_tile(dim, prec, mode);
   if (nt > ctx->sw_ntiles || ctx->sw_epoch >= 0xFFFFu) {
     // fresh (or recycled) look-back words: epoch 0 marks them unpublished
@@ -598,37 +561,6 @@ int run_sweep(sphx_context* ctx, int dim, int prec, int mode, SweepArgs& a, int3
     w.epoch = ++ctx->sw_epoch;
     NvtxRange nvtx_sweep("sphx.pack+sweep");
     ctx->launches += launch_win2(w, st);
-    CKL();
-    if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], st));
-    return SPHX_OK;
-  }
-  if (a.tiled) {
-    TileArgs t;
-    std::memset(&t, 0, sizeof(t));
-    t.n = a.n;
-    t.row0 = a.row0;
-    t.nrows = a.nrows;
-    t.g = a.g;
-    t.c = a.c;
-    for (int k = 0; k < 3; ++k) {
-      t.rel[k] = a.src[k];
-      t.cellk[k] = a.cellk[k];
-    }
-    t.items = a.order;
-    t.start = a.start;
-    t.ids = a.ids;
-    tiled2_shape(a.g.counts[0], a.g.counts[1], a.n, &t.tw, &t.tpr, &t.ntiles);
-    t.cnt = ctx->tl_cnt.as<int32_t>();
-    t.mw = ctx->tl_mw.as<uint32_t>();
-    t.mx = ctx->tl_mx.as<uint32_t>();
-    t.flag = ctx->tl_flag.as<uint8_t>();
-    t.rank = ctx->tl_rank.as<uint32_t>();
-    t.offsets = a.offsets;
-    t.out = d_items;
-    t.capacity = capacity;
-    t.tiles = ctx->sw_tiles.as<unsigned long long>();
-    t.epoch = ++ctx->sw_epoch;
-    ctx->launches += launch_tiled2(t, true, st);
     CKL();
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], st));
     return SPHX_OK;
@@ -838,7 +770,6 @@ void sphx_destroy(sphx_context* ctx) {
                 &ctx->b_out_start, &ctx->b_out_items, &ctx->b_rel[0], &ctx->b_rel[1],
                 &ctx->b_rel[2], &ctx->b_cell[0], &ctx->b_cell[1], &ctx->b_cell[2],
                 &ctx->s_stress, &ctx->s_rates, &ctx->s_dx, &ctx->s_flags,
-                &ctx->tl_cnt, &ctx->tl_mw, &ctx->tl_mx, &ctx->tl_flag, &ctx->tl_rank,
                 &ctx->w_xy, &ctx->w_u, &ctx->w_id, &ctx->w_run};
   for (Buf* b : all) b->release();
   for (auto& ev : ctx->ev)

@@ -67,38 +67,9 @@ struct SweepArgs {
   unsigned long long* xy_tiles;  // scan look-back words + counter (zeroed per call)
   int32_t* rowk;              // [nrows] row lengths of the test pass (bit 31: words overflowed)
   unsigned* hitw;             // [W][nrows] hit words of the test pass
-  int tiled;                  // 2-D FP16 RCLL: the cell-tiled path (tiled.cu), no encode
   int win2;                   // 2-D FP16 RCLL: the windowed path (window.cu), no encode
-  const double* src[3];       // tiled path: RelCoords::rel[k]
-  const int32_t* start;       // tiled path: CellGrid::cell_start
-};
-
-// Cell-tiled FP16 RCLL (tiled.cu). A tile is a run of `tw` cells of one cell
-// row; its CTA stages the CSR segments of the three neighbour rows in shared
-// memory and treats the tile's members as the targets.
-struct TileArgs {
-  int n;                      // particles of the system (CSR size)
-  int row0, nrows;            // rows produced: particles [row0, row0 + nrows)
-  GridConsts g;
-  PrecConsts c;
-  const double* rel[3];       // RelCoords::rel[k] (particle order, FP64)
-  const int32_t* cellk[3];    // RelCoords::cell[k]
-  const int32_t* items;       // CellGrid::items (CSR, ascending ids per cell)
-  const int32_t* start;       // CellGrid::cell_start [C+1]
-  const int32_t* ids;         // output id of particle j (null: j)
-  int tw, tpr;                // tile width in cells, tiles per cell row
-  int64_t ntiles;
-  int32_t* cnt;               // [nrows] row lengths (count pass)
-  uint32_t* mw;               // [3][n] hit words of the 3 row segments (by CSR position)
-  uint32_t* mx;               // [3][n] second hit words (segments of 33..64 entries)
-  uint8_t* flag;              // [n] 1: the row takes the global-memory path
-  uint32_t* rank;             // [n] (by CSR position) byte s: the record's place in the id-merged
-                              //     x-triple centred at its cell's x + s - 1 (count -> fill)
-  int64_t* offsets;           // [nrows + 1]
-  int32_t* out;               // [capacity] neighbour ids
-  int64_t capacity;
-  unsigned long long* tiles;  // scan look-back words (epoch-tagged)
-  unsigned epoch;
+  const double* src[3];       // windowed path: RelCoords::rel[k]
+  const int32_t* start;       // windowed path: CellGrid::cell_start
 };
 
 // Arguments of the windowed 2-D FP16 RCLL (capi.cu fills them).
