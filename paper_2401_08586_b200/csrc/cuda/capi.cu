@@ -52,6 +52,7 @@ int launch_step_rates(int dim, const StepArgs& a, cudaStream_t st);
 int launch_kick_drift(int dim, const StepArgs& a, cudaStream_t st);
 // window.cu
 int64_t win2_tiles(int64_t nrows);
+size_t win2_desc_bytes(int64_t nrows);
 int launch_win2(const Win2Args& a, cudaStream_t st);
 // slab.cu
 int launch_slab_assemble(const SlabArgs& a, cudaStream_t st);
@@ -153,7 +154,7 @@ struct sphx_context {
   // device time step: stress (sigma, tau, eps), rates, displacement, max |dx|, status
   Buf s_stress, s_rates, s_dx, s_flags;
   // windowed 2-D FP16 RCLL: CSR-order binary16 x/y pairs, cell x, ids, run lists
-  Buf w_xy, w_u, w_id, w_run;
+  Buf w_xy, w_u, w_id, w_run, w_desc;
   // pinned staging for pageable host buffers (two chunks) and their events
   void* h_stage = nullptr;
   cudaEvent_t h_ev[2] = {nullptr, nullptr};
@@ -457,6 +458,7 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
         if (b->p != old) CK(cudaMemsetAsync(b->p, 0, b->bytes, st));
       }
       TRY(ctx->w_run.ensure(32 * (size_t)C));
+      TRY(ctx->w_desc.ensure(win2_desc_bytes(nrows)));
       SweepArgs& a = *out;
       a.g = grid_consts(g);
       a.c = pc;
@@ -554,6 +556,7 @@ int run_sweep(sphx_context* ctx, int dim, int prec, int mode, SweepArgs& a, int3
     w.wu = ctx->w_u.as<__half>();
     w.wid = ctx->w_id.as<int32_t>();
     w.wrun = ctx->w_run.as<uint8_t>();
+    w.desc = ctx->w_desc.p;
     w.offsets = a.offsets;
     w.out = d_items;
     w.capacity = capacity;
@@ -770,7 +773,7 @@ void sphx_destroy(sphx_context* ctx) {
                 &ctx->b_out_start, &ctx->b_out_items, &ctx->b_rel[0], &ctx->b_rel[1],
                 &ctx->b_rel[2], &ctx->b_cell[0], &ctx->b_cell[1], &ctx->b_cell[2],
                 &ctx->s_stress, &ctx->s_rates, &ctx->s_dx, &ctx->s_flags,
-                &ctx->w_xy, &ctx->w_u, &ctx->w_id, &ctx->w_run};
+                &ctx->w_xy, &ctx->w_u, &ctx->w_id, &ctx->w_run, &ctx->w_desc};
   for (Buf* b : all) b->release();
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);

@@ -86,6 +86,8 @@ struct Win2Args {
   __half* wu;                 // [n + 16] CSR cell x of each record (binary16)
   int32_t* wid;               // [n + 16] candidate ids (CSR order)
   uint8_t* wrun;              // [C][32] run lists: positions of each x-triple in id order
+  void* desc;                 // [tiles] W2Desc: each tile's bands and window rows (pack -> sweep)
+  int bt, wcap, cscap, runcap;  // the sweep's tile size and shared-memory capacities
   int64_t* offsets;           // [nrows + 1]
   int32_t* out;               // [capacity]
   int64_t capacity;

@@ -64,6 +64,19 @@ constexpr int kRowsMax = 12;  // window rows (both bands)
 constexpr int kBandRows = 6;  // rows of one band: ymax - ymin <= 3
 constexpr int kPackR = 4;     // records per pack thread
 
+// A tile's window, computed by the pack (one warp per tile) and brought into
+// the sweep's shared memory with one bulk copy. fast = 0: no window (the tile's
+// targets do not form <= 2 compact bands, or the window does not fit).
+struct W2Desc {
+  int fast, nb, split, total;  // bands; first row of band 1; window records
+  int bx[2][4];                // band: xmin, xmax, ymin, ymax
+  int rbase[kRowsMax];         // window row: window position of its first record
+  int ra8[kRowsMax];           //   aligned CSR start (-1: no row)
+  int rn[kRowsMax];            //   records (8-aligned)
+  int rgy[kRowsMax];           //   grid row
+};
+static_assert(sizeof(W2Desc) % 16 == 0, "bulk-copied");
+
 template <int BT>
 struct W2Cfg {
   static constexpr int WCap = 12 * BT + BT / 2;  // window records
@@ -231,13 +244,8 @@ struct W2Smem {
   uint4 run[C::RunCap * 2];        // run lists of the window's centre cells (32 bytes each)
   short cs[C::CSCap];              // window cell boundaries, relative to the row's CSR start
   unsigned hw[3][BT];              // phase A hit words of the 3 segments
-  int rbase[kRowsMax];             // row r: window position of its first record
-  int ra8[kRowsMax], rn[kRowsMax]; //   aligned CSR start (-1: no row), records
-  int rgy[kRowsMax];               //   grid row
-  int bx[2][4];                    // band: xmin, xmax, ymin, ymax
-  int last[BT / 32][2];            // warp w's lane 31 cell (x, y)
+  W2Desc d;                        // the tile's bands and window rows (from the pack)
   int wsum[BT / 32];
-  int split, total;
   long long base;
   unsigned long long bar;
 };
@@ -263,7 +271,7 @@ struct GlobSrc {
   __device__ __forceinline__ int ident(int p) const { return __ldg(id + p); }
 };
 
-// Band geometry (identical in every thread: computed from S.bx).
+// Band geometry (identical in every thread: computed from the descriptor).
 struct Geo {
   int rows[2], ncs[2], nrun[2];
   __device__ __forceinline__ int row0(int q) const { return q ? rows[0] : 0; }
@@ -277,6 +285,18 @@ struct Geo {
   }
 };
 
+__device__ __forceinline__ Geo geo_of(const int (&bx)[2][4], int nb) {
+  Geo G;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const bool on = q < nb;
+    G.rows[q] = on ? bx[q][3] - bx[q][2] + 3 : 0;
+    G.ncs[q] = on ? bx[q][1] - bx[q][0] + 4 : 0;
+    G.nrun[q] = on ? bx[q][1] - bx[q][0] + 1 : 0;
+  }
+  return G;
+}
+
 // Segment of target (cx, cy) in stencil row oy = s - 1: window positions of the
 // cell boundaries L | C | R | end, and the window row.
 struct Seg {
@@ -286,9 +306,9 @@ template <int BT>
 __device__ __forceinline__ Seg seg_of(const W2Smem<BT>& S, const Geo& G, int b, int cx, int cy,
                                       int s) {
   Seg g;
-  g.r = G.row0(b) + (cy + s - S.bx[b][2]);  // window row (ymin-1 is the band's row 0)
-  const short* cs = S.cs + G.cs0(g.r) + (cx - S.bx[b][0]);
-  const int base = S.rbase[g.r];
+  g.r = G.row0(b) + (cy + s - S.d.bx[b][2]);  // window row (ymin-1 is the band's row 0)
+  const short* cs = S.cs + G.cs0(g.r) + (cx - S.d.bx[b][0]);
+  const int base = S.d.rbase[g.r];
   g.pL = base + cs[0];
   g.pC = base + cs[1];
   g.pR = base + cs[2];
@@ -327,14 +347,139 @@ __device__ __forceinline__ Seg seg_glob(const Win2Args& a, int cx, int cy, int s
 // block's cells and their x-neighbours are one CSR span, staged in shared
 // memory. Triples whose span exceeds 32 or that need a wrapped cell get no run
 // list (the sweep takes those rows on the exact path).
-__global__ void __launch_bounds__(256) k_w2_pack(Win2Args a, int ncb) {
+// One warp per sweep tile (blocks [0, ntb)): the tile's bands and window rows
+// (the sweep's prologue, moved here where issue slots are idle). Targets are the
+// tile's a.bt consecutive rows, bt/32 per lane; a band split is a jump of more
+// than two cells between consecutive targets.
+__device__ void w2_tile_desc(const Win2Args& a, int tile) {
+  const int lane = threadIdx.x & 31, per = a.bt >> 5;
+  const int nx = a.g.counts[0], ny = a.g.counts[1];
+  const int r0 = tile * a.bt + lane * per;
+  auto cell = [&](int j, int& x, int& y) {  // target r0 + j (false past the rows)
+    if (r0 + j >= a.nrows) return false;
+    const int i = a.row0 + r0 + j;
+    x = __ldg(a.cellk[0] + i);
+    y = __ldg(a.cellk[1] + i);
+    return true;
+  };
+  // breaks between consecutive targets (the previous lane's last for j = 0)
+  int lx = 0, ly = 0;
+  cell(per - 1, lx, ly);
+  int qx = __shfl_up_sync(0xffffffffu, lx, 1), qy = __shfl_up_sync(0xffffffffu, ly, 1);
+  int nbrk = 0, first = INT_MAX;
+  for (int j = 0; j < per; ++j) {
+    int x, y;
+    if (!cell(j, x, y)) break;
+    if ((lane > 0 || j > 0) && (abs(x - qx) > 2 || abs(y - qy) > 2)) {
+      ++nbrk;
+      first = min(first, lane * per + j);
+    }
+    qx = x;
+    qy = y;
+  }
+  nbrk = __reduce_add_sync(0xffffffffu, nbrk);
+  first = __reduce_min_sync(0xffffffffu, first);
+  W2Desc* D = static_cast<W2Desc*>(a.desc) + tile;
+  int fast = nbrk <= 1;
+  const int nb = nbrk + 1, split = nbrk == 1 ? first : a.bt;
+  int bx[2][4];
+  {
+    int x0[2] = {INT_MAX, INT_MAX}, x1[2] = {INT_MIN, INT_MIN};
+    int y0[2] = {INT_MAX, INT_MAX}, y1[2] = {INT_MIN, INT_MIN};
+    for (int j = 0; j < per; ++j) {  // (the cells are L1 hits now)
+      int x, y;
+      if (!cell(j, x, y)) break;
+      const bool q1 = lane * per + j >= split;
+      x0[0] = q1 ? x0[0] : min(x0[0], x);
+      x1[0] = q1 ? x1[0] : max(x1[0], x);
+      y0[0] = q1 ? y0[0] : min(y0[0], y);
+      y1[0] = q1 ? y1[0] : max(y1[0], y);
+      x0[1] = q1 ? min(x0[1], x) : x0[1];
+      x1[1] = q1 ? max(x1[1], x) : x1[1];
+      y0[1] = q1 ? min(y0[1], y) : y0[1];
+      y1[1] = q1 ? max(y1[1], y) : y1[1];
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      bx[q][0] = __reduce_min_sync(0xffffffffu, x0[q]);
+      bx[q][1] = __reduce_max_sync(0xffffffffu, x1[q]);
+      bx[q][2] = __reduce_min_sync(0xffffffffu, y0[q]);
+      bx[q][3] = __reduce_max_sync(0xffffffffu, y1[q]);
+    }
+  }
+  const Geo G = geo_of(bx, fast ? nb : 0);
+  if (fast) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (q >= nb) continue;
+      // rows/cells of the band inside the grid; columns xmin-1 .. xmax+1 must not
+      // wrap a periodic x axis
+      if (bx[q][0] < 0 || bx[q][1] >= nx || bx[q][2] < 0 || bx[q][3] >= ny) fast = 0;
+      if (a.g.wrap[0] && (bx[q][0] == 0 || bx[q][1] == nx - 1)) fast = 0;
+      if (G.rows[q] > kBandRows) fast = 0;
+    }
+    const int nr = G.rows[0] + G.rows[1];
+    if (G.cs0(nr) > a.cscap || G.run0(nr) > a.runcap) fast = 0;
+  }
+  // window rows: one lane per row
+  const int nrw = fast ? G.rows[0] + G.rows[1] : 0;
+  int gy = -1, a8 = -1, n8 = 0;
+  if (lane < nrw) {
+    const int q = lane < G.rows[0] ? 0 : 1;
+    const int bx0 = q ? bx[1][0] : bx[0][0], bx1 = q ? bx[1][1] : bx[0][1];
+    const int y = (q ? bx[1][2] : bx[0][2]) - 1 + (lane - G.row0(q));
+    gy = y;
+    if (y < 0 || y >= ny) gy = a.g.wrap[1] ? (y + ny) % ny : -1;
+    if (gy >= 0) {
+      const int64_t row = (int64_t)gy * nx;
+      const int s0 = __ldg(a.start + row + max(bx0 - 1, 0));
+      const int s1 = __ldg(a.start + row + min(bx1 + 1, nx - 1) + 1);
+      a8 = s0 & ~7;
+      n8 = s1 > s0 ? ((s1 + 7) & ~7) - a8 : 0;
+    }
+  }
+  int incl = n8;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  if (total > a.wcap) fast = 0;
+  if (lane < kRowsMax) {
+    D->rbase[lane] = incl - n8;
+    D->ra8[lane] = a8;
+    D->rn[lane] = n8;
+    D->rgy[lane] = gy;
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) D->bx[q][e] = bx[q][e];
+  }
+  if (lane == 0) {
+    D->fast = fast;
+    D->nb = nb;
+    D->split = split;
+    D->total = total;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_w2_pack(Win2Args a, int ntb, int ncb) {
   const int tid = threadIdx.x;
-  if ((int)blockIdx.x < ncb) {
+  if ((int)blockIdx.x < ntb) {
+    const int tile = blockIdx.x * 8 + (tid >> 5);
+    if (tile * a.bt < a.nrows) w2_tile_desc(a, tile);
+    pdl_trigger();
+    return;
+  }
+  if ((int)blockIdx.x < ntb + ncb) {
     constexpr int kSpan = 2048;
     __shared__ int sid[kSpan];
     __shared__ int sst[256 + 3];
     const int64_t C = (int64_t)a.g.counts[0] * a.g.counts[1];
-    const int64_t v0 = (int64_t)blockIdx.x * 256;
+    const int64_t v0 = (int64_t)(blockIdx.x - ntb) * 256;
     for (int e = tid; e < 256 + 3; e += 256)
       sst[e] = __ldg(a.start + min(max(v0 - 1 + e, (int64_t)0), C));
     __syncthreads();
@@ -388,7 +533,7 @@ __global__ void __launch_bounds__(256) k_w2_pack(Win2Args a, int ncb) {
   }
   int id[kPackR];
   double rx[kPackR], ry[kPackR];
-  const int s0 = (blockIdx.x - ncb) * 256 * kPackR + tid;
+  const int s0 = (blockIdx.x - ntb - ncb) * 256 * kPackR + tid;
 #pragma unroll
   for (int q = 0; q < kPackR; ++q) {
     const int s = s0 + 256 * q;
@@ -471,141 +616,62 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
   const int r = tile * BT + tid;
   const bool valid = r < a.nrows;
   const int i = a.row0 + (valid ? r : 0);
-  const int nx = a.g.counts[0], ny = a.g.counts[1];
+  const int nx = a.g.counts[0];
   const uint32_t bar = smem_u32(&S.bar);
 
-  // ---- targets (inputs only: overlaps the pack's tail) ----
+  // ---- targets (inputs: issued before the pack is waited for) ----
   const int cx = __ldg(a.cellk[0] + i), cy = __ldg(a.cellk[1] + i);
   const __half rxh = __double2half(__ldg(a.rel[0] + i));
   const __half ryh = __double2half(__ldg(a.rel[1] + i));
 
-  // ---- bands: split the tile where consecutive targets jump > 2 cells ----
-  if (lane == 31) {
-    S.last[warp][0] = cx;
-    S.last[warp][1] = cy;
-  }
+  // ---- the tile's descriptor (bands, window rows: the pack's tile warps) ----
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    S.split = BT;
-    S.total = 0;
-    S.bx[0][0] = S.bx[1][0] = INT_MAX;
-    S.bx[0][1] = S.bx[1][1] = INT_MIN;
-    S.bx[0][2] = S.bx[1][2] = INT_MAX;
-    S.bx[0][3] = S.bx[1][3] = INT_MIN;
+    pdl_wait();  // the pack's arrays are complete
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                 "r"((unsigned)sizeof(W2Desc))
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(&S.d)),
+        "l"(static_cast<const W2Desc*>(a.desc) + tile), "r"((unsigned)sizeof(W2Desc)), "r"(bar)
+        : "memory");
   }
-  __syncthreads();
-  int pcx = __shfl_up_sync(0xffffffffu, cx, 1), pcy = __shfl_up_sync(0xffffffffu, cy, 1);
-  if (lane == 0 && warp > 0) {
-    pcx = S.last[warp - 1][0];
-    pcy = S.last[warp - 1][1];
-  }
-  const bool brk = valid && tid > 0 && (abs(cx - pcx) > 2 || abs(cy - pcy) > 2);
-  if (brk) atomicMin(&S.split, tid);  // read only when there is exactly one break
-  const int nbrk = __syncthreads_count(brk);
-  bool fast = nbrk <= 1;
-  const int b = (nbrk == 1 && tid >= S.split) ? 1 : 0;
-  if (fast) {
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const bool in = valid && b == q;
-      const int x0 = __reduce_min_sync(0xffffffffu, in ? cx : INT_MAX);
-      const int x1 = __reduce_max_sync(0xffffffffu, in ? cx : INT_MIN);
-      const int y0 = __reduce_min_sync(0xffffffffu, in ? cy : INT_MAX);
-      const int y1 = __reduce_max_sync(0xffffffffu, in ? cy : INT_MIN);
-      if (lane == 0 && x0 != INT_MAX) {
-        atomicMin(&S.bx[q][0], x0);
-        atomicMax(&S.bx[q][1], x1);
-        atomicMin(&S.bx[q][2], y0);
-        atomicMax(&S.bx[q][3], y1);
-      }
-    }
-  }
-  __syncthreads();
-
-  // ---- window geometry (uniform) ----
-  Geo G{};
-  if (fast) {
-    const int nb = nbrk + 1;
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const bool on = q < nb;
-      G.rows[q] = on ? S.bx[q][3] - S.bx[q][2] + 3 : 0;
-      G.ncs[q] = on ? S.bx[q][1] - S.bx[q][0] + 4 : 0;
-      G.nrun[q] = on ? S.bx[q][1] - S.bx[q][0] + 1 : 0;
-      if (on) {
-        // rows/cells of the band inside the grid; columns xmin-1 .. xmax+1 must
-        // not wrap a periodic x axis
-        if (S.bx[q][0] < 0 || S.bx[q][1] >= nx || S.bx[q][2] < 0 || S.bx[q][3] >= ny) fast = false;
-        if (a.g.wrap[0] && (S.bx[q][0] == 0 || S.bx[q][1] == nx - 1)) fast = false;
-        if (G.rows[q] > kBandRows) fast = false;
-      }
-    }
-    if (G.cs0(G.rows[0] + G.rows[1]) > Cfg::CSCap || G.run0(G.rows[0] + G.rows[1]) > Cfg::RunCap)
-      fast = false;
-  }
-
-  // ---- window rows (cell_start is an input): a warp per row ----
+  // one warp polls the barrier (phase `ph`); the others wait at __syncthreads
+  auto wait_bar = [&](unsigned ph) {
+    if (warp == 0)
+      asm volatile(
+          "{\n\t.reg .pred P;\n"
+          "W2WAIT%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+          "@!P bra W2WAIT%=;\n\t}" ::"r"(bar),
+          "r"(ph)
+          : "memory");
+    __syncthreads();
+  };
+  wait_bar(0);
+  bool fast = S.d.fast;
+  const int b = (S.d.nb == 2 && tid >= S.d.split) ? 1 : 0;
+  const Geo G = geo_of(S.d.bx, fast ? S.d.nb : 0);
   const int nrw = G.rows[0] + G.rows[1];
-  if (fast) {
-    for (int rr = warp; rr < nrw; rr += BT / 32) {
-      const int q = rr < G.rows[0] ? 0 : 1;
-      const int y = S.bx[q][2] - 1 + (rr - G.row0(q));
-      int gy = y;
-      if (y < 0 || y >= ny) gy = a.g.wrap[1] ? (y + ny) % ny : -1;
-      const int ncs = G.ncs_of(q), cs0 = G.cs0(rr);
-      if (gy < 0) {
-        for (int e = lane; e < ncs; e += 32) S.cs[cs0 + e] = 0;
-        if (lane == 0) {
-          S.ra8[rr] = -1;
-          S.rn[rr] = 0;
-          S.rgy[rr] = -1;
-        }
-        continue;
-      }
-      const int64_t row = (int64_t)gy * nx;
-      const int xl = max(S.bx[q][0] - 1, 0), xh = min(S.bx[q][1] + 1, nx - 1);
-      const int s0 = __ldg(a.start + row + xl), s1 = __ldg(a.start + row + xh + 1);
-      const int a8 = s0 & ~7;
-      for (int e = lane; e < ncs; e += 32)
-        S.cs[cs0 + e] = (short)(__ldg(a.start + row + min(max(S.bx[q][0] - 1 + e, 0), nx)) - a8);
-      if (lane == 0) {
-        const int nrec = s1 > s0 ? ((s1 + 7) & ~7) - a8 : 0;
-        S.ra8[rr] = a8;
-        S.rn[rr] = nrec;
-        S.rgy[rr] = gy;
-        atomicAdd(&S.total, nrec);
-      }
-    }
-  }
-  __syncthreads();
-  fast = fast && S.total <= Cfg::WCap;
 
-  // ---- stage the window: TMA bulk copies, one mbarrier ----
-  if (fast && warp == 0) {
-    const int nr = lane < nrw ? S.rn[lane] : 0;
-    int incl = nr;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    if (lane < nrw) S.rbase[lane] = incl - nr;
-    __syncwarp();
-    if (lane == 0) {
-      pdl_wait();  // the pack's arrays are complete
-      unsigned tx = (unsigned)S.total * 10u;
+  // ---- stage the window (TMA bulk copies) while the warps fill the cell
+  // boundaries (cell_start is an input): a warp per row ----
+  if (fast) {
+    if (tid == 0) {
+      unsigned tx = (unsigned)S.d.total * 10u;
       for (int rr = 0; rr < nrw; ++rr)
-        if (S.rgy[rr] >= 0) tx += 32u * (unsigned)G.nrun_of(rr < G.rows[0] ? 0 : 1);
+        if (S.d.rgy[rr] >= 0) tx += 32u * (unsigned)G.nrun_of(rr < G.rows[0] ? 0 : 1);
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx)
                    : "memory");
       for (int rr = 0; rr < nrw; ++rr) {
-        const int gy = S.rgy[rr];
+        const int gy = S.d.rgy[rr];
         if (gy < 0) continue;
         const int q = rr < G.rows[0] ? 0 : 1;
-        const int n8 = S.rn[rr], a8 = S.ra8[rr], wb = S.rbase[rr];
+        const int n8 = S.d.rn[rr], a8 = S.d.ra8[rr], wb = S.d.rbase[rr];
         const void* src[4] = {a.wxy + 2 * (int64_t)a8, a.wu + a8, a.wid + a8,
-                              a.wrun + ((int64_t)gy * nx + S.bx[q][0]) * kSegMax};
+                              a.wrun + ((int64_t)gy * nx + S.d.bx[q][0]) * kSegMax};
         const uint32_t dst[4] = {smem_u32(&S.c.xy[wb >> 1]), smem_u32(&S.c.u[wb]),
                                  smem_u32(&S.id[wb]), smem_u32(&S.run[2 * G.run0(rr)])};
         const unsigned bytes[4] = {4u * n8, 2u * n8, 4u * n8, 32u * (unsigned)G.nrun_of(q)};
@@ -620,17 +686,17 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
         }
       }
     }
-  }
-  if (fast) {
-    // one warp polls the barrier; the others wait at __syncthreads (no issue slots)
-    if (warp == 0)
-      asm volatile(
-          "{\n\t.reg .pred P;\n"
-          "W2WAIT:\n\t"
-          "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n\t"
-          "@!P bra W2WAIT;\n\t}" ::"r"(bar)
-          : "memory");
-    __syncthreads();
+    for (int rr = warp; rr < nrw; rr += BT / 32) {
+      const int q = rr < G.rows[0] ? 0 : 1;
+      const int ncs = G.ncs_of(q), cs0 = G.cs0(rr);
+      const int gy = S.d.rgy[rr], a8 = S.d.ra8[rr];
+      const int64_t row = (int64_t)gy * nx;
+      for (int e = lane; e < ncs; e += 32)
+        S.cs[cs0 + e] =
+            gy < 0 ? (short)0
+                   : (short)(__ldg(a.start + row + min(max(S.d.bx[q][0] - 1 + e, 0), nx)) - a8);
+    }
+    wait_bar(1);
   }
   pdl_wait();  // (the exact path reads the pack's arrays from global memory)
 
@@ -736,7 +802,7 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
       const unsigned hrel = H >> (pL & 1);  // bit o = position pL + o
       uint4 w[2];
       if (fast) {
-        const uint4* rl = &S.run[2 * (H ? G.run0(g.r) + cx - S.bx[b][0] : 0)];
+        const uint4* rl = &S.run[2 * (H ? G.run0(g.r) + cx - S.d.bx[b][0] : 0)];
         w[0] = rl[0];
         w[1] = rl[1];
       } else {
@@ -832,13 +898,21 @@ void launch_sweep_bt(const Win2Args& a, cudaStream_t st) {
 }  // namespace
 
 int64_t win2_tiles(int64_t nrows) { return (nrows + w2_bt() - 1) / w2_bt(); }
+size_t win2_desc_bytes(int64_t nrows) { return sizeof(W2Desc) * (size_t)win2_tiles(nrows); }
 
 // pack + sweep; returns the number of kernels launched
-int launch_win2(const Win2Args& a, cudaStream_t st) {
+int launch_win2(const Win2Args& args, cudaStream_t st) {
+  Win2Args a = args;
+  a.bt = w2_bt();
+  a.wcap = a.bt == 256 ? W2Cfg<256>::WCap : W2Cfg<128>::WCap;
+  a.cscap = a.bt == 256 ? W2Cfg<256>::CSCap : W2Cfg<128>::CSCap;
+  a.runcap = a.bt == 256 ? W2Cfg<256>::RunCap : W2Cfg<128>::RunCap;
   const int nbr = (a.n + 256 * kPackR - 1) / (256 * kPackR);
   const int64_t C = (int64_t)a.g.counts[0] * a.g.counts[1];
   const int ncb = (int)((C + 255) / 256);
-  k_w2_pack<<<(unsigned)(ncb + nbr), 256, 0, st>>>(a, ncb);
+  const int64_t ntiles = (a.nrows + a.bt - 1) / a.bt;
+  const int ntb = (int)((ntiles + 7) / 8);
+  k_w2_pack<<<(unsigned)(ntb + ncb + nbr), 256, 0, st>>>(a, ntb, ncb);
   if (w2_bt() == 256) launch_sweep_bt<256>(a, st);
   else launch_sweep_bt<128>(a, st);
   return 2;
