@@ -254,13 +254,23 @@ struct W2Smem {
 // window positions) or the pack's CSR-order arrays (global memory, CSR
 // positions; tiles without a window). Positions keep their parity in both, so
 // pair p/2 is the same record pair.
-struct SmemSrc {
-  const uint2* xy;
-  const unsigned* u;
-  const int* id;
-  __device__ __forceinline__ uint2 pair(int q) const { return xy[q]; }
-  __device__ __forceinline__ unsigned upair(int q) const { return u[q]; }
-  __device__ __forceinline__ int ident(int p) const { return id[p]; }
+struct SmemSrc {  // 32-bit shared addresses of the window's arrays
+  uint32_t xy, u, id;
+  __device__ __forceinline__ uint2 pair(int q) const {
+    uint2 v;
+    asm("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(xy + 8u * (uint32_t)q));
+    return v;
+  }
+  __device__ __forceinline__ unsigned upair(int q) const {
+    unsigned v;
+    asm("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(u + 4u * (uint32_t)q));
+    return v;
+  }
+  __device__ __forceinline__ int ident(int p) const {
+    int v;
+    asm("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(id + 4u * (uint32_t)p));
+    return v;
+  }
 };
 struct GlobSrc {
   const uint2* xy;
@@ -617,7 +627,14 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
   const bool valid = r < a.nrows;
   const int i = a.row0 + (valid ? r : 0);
   const int nx = a.g.counts[0];
-  const uint32_t bar = smem_u32(&S.bar);
+  // the shared window's base, kept in a register (otherwise re-derived from the
+  // CTA id at every shared access)
+  uint32_t smb = smem_u32(smraw);
+  asm volatile("" : "+r"(smb));
+  auto sa = [&](const void* p) {
+    return smb + (uint32_t)(reinterpret_cast<const unsigned char*>(p) - smraw);
+  };
+  const uint32_t bar = sa(&S.bar);
 
   // ---- targets (inputs: issued before the pack is waited for) ----
   const int cx = __ldg(a.cellk[0] + i), cy = __ldg(a.cellk[1] + i);
@@ -634,7 +651,7 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
                  : "memory");
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(&S.d)),
+            sa(&S.d)),
         "l"(static_cast<const W2Desc*>(a.desc) + tile), "r"((unsigned)sizeof(W2Desc)), "r"(bar)
         : "memory");
   }
@@ -672,8 +689,8 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
         const int n8 = S.d.rn[rr], a8 = S.d.ra8[rr], wb = S.d.rbase[rr];
         const void* src[4] = {a.wxy + 2 * (int64_t)a8, a.wu + a8, a.wid + a8,
                               a.wrun + ((int64_t)gy * nx + S.d.bx[q][0]) * kSegMax};
-        const uint32_t dst[4] = {smem_u32(&S.c.xy[wb >> 1]), smem_u32(&S.c.u[wb]),
-                                 smem_u32(&S.id[wb]), smem_u32(&S.run[2 * G.run0(rr)])};
+        const uint32_t dst[4] = {sa(&S.c.xy[wb >> 1]), sa(&S.c.u[wb]), sa(&S.id[wb]),
+                                 sa(&S.run[2 * G.run0(rr)])};
         const unsigned bytes[4] = {4u * n8, 2u * n8, 4u * n8, 32u * (unsigned)G.nrun_of(q)};
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -707,7 +724,7 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
   const __half2 ut2 = __half2half2(__int2half_rn(cx));
   bool slow = !valid;
   int k = 0;
-  const SmemSrc ssrc{S.c.xy, reinterpret_cast<const unsigned*>(S.c.u), S.id};
+  const SmemSrc ssrc{sa(S.c.xy), sa(S.c.u), sa(S.id)};
   const GlobSrc gsrc{reinterpret_cast<const uint2*>(a.wxy), reinterpret_cast<const unsigned*>(a.wu),
                      a.wid};
   // segment s of this lane's target: window positions (fast tile) or CSR
@@ -834,7 +851,7 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
   };
   const bool fits = btot <= Cfg::PCap;
   if (fits) {
-    const SharedRow row{smem_u32(S.pk) + 4u * (uint32_t)excl};
+    const SharedRow row{sa(S.pk) + 4u * (uint32_t)excl};
     build(row, valid && !slow);
     if (valid && slow && k > 0) w2_slow_row<true>(a, i, cx, cy, rxh, ryh, row);
   }
@@ -855,7 +872,7 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
     if (valid && slow && k > 0) w2_slow_row<true>(a, i, cx, cy, rxh, ryh, row);
     return;
   }
-  stream_tile<BT>(gout, SharedRow{smem_u32(S.pk)}, btot, tid);
+  stream_tile<BT>(gout, SharedRow{sa(S.pk)}, btot, tid);
 }
 
 template <typename... KArgs, typename... Args>
