@@ -53,7 +53,7 @@ int launch_kick_drift(int dim, const StepArgs& a, cudaStream_t st);
 // window.cu
 int64_t win2_tiles(int64_t nrows);
 size_t win2_desc_bytes(int64_t nrows);
-int launch_win2(const Win2Args& a, cudaStream_t st);
+int launch_win2(const Win2Args& a, bool grad, cudaStream_t st);
 // slab.cu
 int launch_slab_assemble(const SlabArgs& a, cudaStream_t st);
 }  // namespace sphx_dev
@@ -518,6 +518,29 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
   return SPHX_OK;
 }
 
+// The windowed 2-D FP16 RCLL kernels' arguments (window.cu) from a prepared call.
+Win2Args win2_args(sphx_context* ctx, const SweepArgs& a) {
+  Win2Args w;
+  std::memset(&w, 0, sizeof(w));
+  w.n = a.n;
+  w.row0 = a.row0;
+  w.nrows = a.nrows;
+  w.g = a.g;
+  w.c = a.c;
+  for (int k = 0; k < 2; ++k) {
+    w.rel[k] = a.src[k];
+    w.cellk[k] = a.cellk[k];
+  }
+  w.items = a.order;
+  w.start = a.start;
+  w.wxy = ctx->w_xy.as<__half>();
+  w.wu = ctx->w_u.as<__half>();
+  w.wid = ctx->w_id.as<int32_t>();
+  w.wrun = ctx->w_run.as<uint8_t>();
+  w.desc = ctx->w_desc.p;
+  return w;
+}
+
 // The single-pass sweep: offsets (always) and the rows (where they fit in
 // `capacity`; the exact total is d_off[nrows] either way).
 int run_sweep(sphx_context* ctx, int dim, int prec, int mode, SweepArgs& a, int32_t* d_items,
@@ -539,31 +562,14 @@ int run_sweep(sphx_context* ctx, int dim, int prec, int mode, SweepArgs& a, int3
     ctx->sw_tick = 0;
   }
   if (a.win2) {
-    Win2Args w;
-    std::memset(&w, 0, sizeof(w));
-    w.n = a.n;
-    w.row0 = a.row0;
-    w.nrows = a.nrows;
-    w.g = a.g;
-    w.c = a.c;
-    for (int k = 0; k < 2; ++k) {
-      w.rel[k] = a.src[k];
-      w.cellk[k] = a.cellk[k];
-    }
-    w.items = a.order;
-    w.start = a.start;
-    w.wxy = ctx->w_xy.as<__half>();
-    w.wu = ctx->w_u.as<__half>();
-    w.wid = ctx->w_id.as<int32_t>();
-    w.wrun = ctx->w_run.as<uint8_t>();
-    w.desc = ctx->w_desc.p;
+    Win2Args w = win2_args(ctx, a);
     w.offsets = a.offsets;
     w.out = d_items;
     w.capacity = capacity;
     w.tiles = ctx->sw_tiles.as<unsigned long long>();
     w.epoch = ++ctx->sw_epoch;
     NvtxRange nvtx_sweep("sphx.pack+sweep");
-    ctx->launches += launch_win2(w, st);
+    ctx->launches += launch_win2(w, false, st);
     CKL();
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], st));
     return SPHX_OK;
@@ -1243,8 +1249,27 @@ int sphx_rcll_grad_normalized_device(sphx_context* ctx, const sphx_grid_desc* gr
   ctx->t_n = -1;
   ctx->t_rcll = false;
   TRY(ctx->t_offsets.ensure(sizeof(int64_t) * (n + 1)));
+  // 2-D: the windowed kernels (window.cu) with the gradient in place of the
+  // table; 3-D (and grids the window does not cover): encode + k_r16_grad
   TRY(run_prepare(ctx, MODE_RCLL, *grid, n, d_rel, d_cell, d_items, d_cell_start, nullptr,
-                  precision, 0.0, ctx->t_offsets.as<int64_t>(), &a, RowSel(), false));
+                  precision, 0.0, ctx->t_offsets.as<int64_t>(), &a, RowSel(), grid->dim == 2));
+  const double pi_ = 3.141592653589793;
+  if (a.win2) {
+    Win2Args w = win2_args(ctx, a);
+    for (int k = 0; k < 2; ++k) {
+      w.gx[k] = d_x[k];
+      w.gout[k] = d_g[k];
+    }
+    w.gf = d_f;
+    w.gdeg = d_degenerate;
+    w.gh = h;
+    w.galpha = 15.0 / (7.0 * pi_ * h * h);  // make_kernel (kernel.hpp:17-29), dim 2
+    NvtxRange nvtx_grad("sphx.pack+grad");
+    ctx->launches += launch_win2(w, true, ctx->stream);
+    CKL();
+    if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], ctx->stream));
+    return SPHX_OK;
+  }
   for (int k = 0; k < 3; ++k) {
     a.gx[k] = k < grid->dim ? d_x[k] : nullptr;
     a.gout[k] = k < grid->dim ? d_g[k] : nullptr;

@@ -88,6 +88,12 @@ struct Win2Args {
   uint8_t* wrun;              // [C][32] run lists: positions of each x-triple in id order
   void* desc;                 // [tiles] W2Desc: each tile's bands and window rows (pack -> sweep)
   int bt, wcap, cscap, runcap;  // the sweep's tile size and shared-memory capacities
+  // fused NNPS -> grad_normalized (gradient.cpp:44-82): no table, g per particle
+  const double* gx[2];        // ParticleSystem::x(k)
+  const double* gf;           // the field f
+  double* gout[2];            // GradField::g[k]
+  unsigned long long* gdeg;   // GradField::degenerate_count (accumulated)
+  double gh, galpha;          // KernelParams h, alpha (make_kernel, kernel.hpp:17-29)
   int64_t* offsets;           // [nrows + 1]
   int32_t* out;               // [capacity]
   int64_t capacity;

@@ -576,7 +576,7 @@ __device__ __forceinline__ __half w2_y(const Win2Args& a, int64_t s) {
 // The exact per-row path (any input): the reference's 9-cell walk
 // (nnps.cpp:354-410) with its minimum-image offsets dc = -off (:359-362).
 // EMIT: the row is written to dst[0, k) and sorted.
-template <bool EMIT, class Row>
+template <bool EMIT, class Row, bool SORT = true>
 __device__ int w2_slow_row(const Win2Args& a, int i, int cxi, int cyi, __half rx, __half ry,
                            const Row& dst) {
   const int nx = a.g.counts[0], ny = a.g.counts[1];
@@ -612,11 +612,86 @@ __device__ int w2_slow_row(const Win2Args& a, int i, int cxi, int cyi, __half rx
       }
     }
   }
-  if (EMIT) insertion_sort(dst, k);
+  if (EMIT && SORT) insertion_sort(dst, k);
   return k;
 }
 
-template <int BT>
+// grad_normalized's per-row sums (gradient.cpp:57-72, kernel_grad kernel.hpp:
+// 53-64, kernel_dwdr :40-47) in the reference's operation order, every FP64 op
+// rounded once (no contraction), over the row's neighbours in ascending id order.
+__device__ __forceinline__ double w2_dwdr(double R, double alpha) {
+  if (R < 1.0) return __dmul_rn(alpha, __dadd_rn(__dmul_rn(-2.0, R), __dmul_rn(__dmul_rn(1.5, R), R)));
+  if (R < 2.0) {
+    const double t = __dsub_rn(2.0, R);
+    return __dmul_rn(-alpha, __dmul_rn(__dmul_rn(0.5, t), t));
+  }
+  return 0.0;
+}
+struct W2Grad {
+  double num[2] = {0.0, 0.0}, den[2] = {0.0, 0.0}, scale[2] = {0.0, 0.0};
+  double xi[2], fi;
+  __device__ __forceinline__ void add(const Win2Args& a, int j) {
+    double dx[2], gw[2] = {0.0, 0.0}, r2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      dx[k] = __dsub_rn(xi[k], __ldg(a.gx[k] + j));
+      r2 = __dadd_rn(r2, __dmul_rn(dx[k], dx[k]));
+    }
+    const double r = __dsqrt_rn(r2);
+    if (r != 0.0) {
+      const double R = __ddiv_rn(r, a.gh);
+      const double sc = __ddiv_rn(w2_dwdr(R, a.galpha), __dmul_rn(a.gh, r));
+#pragma unroll
+      for (int k = 0; k < 2; ++k) gw[k] = __dmul_rn(sc, dx[k]);
+    }
+    const double df = __dsub_rn(__ldg(a.gf + j), fi);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      num[k] = __dadd_rn(num[k], __dmul_rn(df, gw[k]));
+      den[k] = __dadd_rn(den[k], __dmul_rn(-dx[k], gw[k]));
+      scale[k] = __dadd_rn(scale[k], fabs(__dmul_rn(dx[k], gw[k])));
+    }
+  }
+  // g_k = num/den, or 0 and a degenerate count (gradient.cpp:73-80)
+  __device__ __forceinline__ unsigned long long finish(const Win2Args& a, int i) const {
+    unsigned long long deg = 0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const double lim = __dmul_rn(1e-14, scale[k] > 0.0 ? scale[k] : 1.0);
+      double g = 0.0;
+      if (fabs(den[k]) < lim) ++deg;
+      else g = __ddiv_rn(num[k], den[k]);
+      a.gout[k][i] = g;
+    }
+    return deg;
+  }
+};
+
+// The gradient of a row that is not packed in shared memory: its neighbours in
+// ascending id order by repeated selection over the exact 9-cell walk.
+__device__ void w2_slow_grad(const Win2Args& a, int i, int cxi, int cyi, __half rx, __half ry,
+                             W2Grad& acc) {
+  int last = INT_MIN;
+  while (true) {
+    int best = INT_MAX;
+    const struct Sel {
+      int* best;
+      int last;
+      __device__ void st(int, int v) const {
+        if (v > last && v < *best) *best = v;
+      }
+      __device__ int ld(int) const { return 0; }
+    } sel{&best, last};
+    w2_slow_row<true, Sel, false>(a, i, cxi, cyi, rx, ry, sel);
+    if (best == INT_MAX) break;
+    acc.add(a, best);
+    last = best;
+  }
+}
+
+// GRAD: the fused NNPS -> grad_normalized (no table): each packed row is walked
+// in id order into the FP64 sums of its particle.
+template <int BT, bool GRAD>
 __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
   using Cfg = W2Cfg<BT>;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -801,7 +876,7 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
     btot += S.wsum[u];
   }
   const int excl = wbase + incl - k;
-  if (tid == 0) lb_publish(a.tiles, tile, btot, a.epoch);
+  if (!GRAD && tid == 0) lb_publish(a.tiles, tile, btot, a.epoch);
 
   // ---- B: sorted rows ----
   // The run list of the target's centre cell walks each segment in id order, so
@@ -855,6 +930,26 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
     build(row, valid && !slow);
     if (valid && slow && k > 0) w2_slow_row<true>(a, i, cx, cy, rxh, ryh, row);
   }
+  if constexpr (GRAD) {
+    unsigned long long deg = 0;
+    if (valid) {
+      W2Grad acc;
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) acc.xi[kk] = __ldg(a.gx[kk] + i);
+      acc.fi = __ldg(a.gf + i);
+      if (fits) {  // the thread's own sorted row
+        const SharedRow row{sa(S.pk) + 4u * (uint32_t)excl};
+        for (int e = 0; e < k; ++e) acc.add(a, row.ld(e));
+      } else {
+        w2_slow_grad(a, i, cx, cy, rxh, ryh, acc);
+      }
+      deg = acc.finish(a, i);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) deg += __shfl_xor_sync(0xffffffffu, deg, o);
+    if (lane == 0 && deg) atomicAdd(a.gdeg, deg);
+    return;
+  }
 
   if (warp == 0) {
     const long long bse = lb_resolve(a.tiles, tile, btot, a.epoch);
@@ -901,15 +996,15 @@ int w2_bt() {
   return bt;
 }
 
-template <int BT>
+template <int BT, bool GRAD>
 void launch_sweep_bt(const Win2Args& a, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_w2<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_w2<BT, GRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(W2Smem<BT>));
     attr = true;
   }
-  launch_pdl(k_w2<BT>, (unsigned)((a.nrows + BT - 1) / BT), BT, sizeof(W2Smem<BT>), st, a);
+  launch_pdl(k_w2<BT, GRAD>, (unsigned)((a.nrows + BT - 1) / BT), BT, sizeof(W2Smem<BT>), st, a);
 }
 
 }  // namespace
@@ -917,8 +1012,8 @@ void launch_sweep_bt(const Win2Args& a, cudaStream_t st) {
 int64_t win2_tiles(int64_t nrows) { return (nrows + w2_bt() - 1) / w2_bt(); }
 size_t win2_desc_bytes(int64_t nrows) { return sizeof(W2Desc) * (size_t)win2_tiles(nrows); }
 
-// pack + sweep; returns the number of kernels launched
-int launch_win2(const Win2Args& args, cudaStream_t st) {
+// pack + sweep (grad: pack + fused gradient); returns the number of kernels launched
+int launch_win2(const Win2Args& args, bool grad, cudaStream_t st) {
   Win2Args a = args;
   a.bt = w2_bt();
   a.wcap = a.bt == 256 ? W2Cfg<256>::WCap : W2Cfg<128>::WCap;
@@ -930,8 +1025,13 @@ int launch_win2(const Win2Args& args, cudaStream_t st) {
   const int64_t ntiles = (a.nrows + a.bt - 1) / a.bt;
   const int ntb = (int)((ntiles + 7) / 8);
   k_w2_pack<<<(unsigned)(ntb + ncb + nbr), 256, 0, st>>>(a, ntb, ncb);
-  if (w2_bt() == 256) launch_sweep_bt<256>(a, st);
-  else launch_sweep_bt<128>(a, st);
+  if (grad) {
+    if (a.bt == 256) launch_sweep_bt<256, true>(a, st);
+    else launch_sweep_bt<128, true>(a, st);
+  } else {
+    if (a.bt == 256) launch_sweep_bt<256, false>(a, st);
+    else launch_sweep_bt<128, false>(a, st);
+  }
   return 2;
 }
 
