@@ -53,7 +53,7 @@ int launch_kick_drift(int dim, const StepArgs& a, cudaStream_t st);
 // window.cu
 int64_t win2_tiles(int64_t nrows);
 size_t win2_desc_bytes(int64_t nrows);
-int launch_win2(const Win2Args& a, bool grad, cudaStream_t st);
+int launch_win2(const Win2Args& a, bool grad, cudaStream_t st, cudaEvent_t mid);
 // slab.cu
 int launch_slab_assemble(const SlabArgs& a, cudaStream_t st);
 }  // namespace sphx_dev
@@ -469,10 +469,7 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
       }
       a.start = start;
       a.cell_of = cell_of;
-      if (ctx->timing) {
-        CK(cudaEventRecord(ctx->ev[0], st));
-        CK(cudaEventRecord(ctx->ev[1], st));
-      }
+      if (ctx->timing) CK(cudaEventRecord(ctx->ev[0], st));  // ev[1]: after the pack
       return SPHX_OK;
     }
   }
@@ -569,7 +566,7 @@ int run_sweep(sphx_context* ctx, int dim, int prec, int mode, SweepArgs& a, int3
     w.tiles = ctx->sw_tiles.as<unsigned long long>();
     w.epoch = ++ctx->sw_epoch;
     NvtxRange nvtx_sweep("sphx.pack+sweep");
-    ctx->launches += launch_win2(w, false, st);
+    ctx->launches += launch_win2(w, false, st, ctx->timing ? ctx->ev[1] : nullptr);
     CKL();
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], st));
     return SPHX_OK;
@@ -1265,7 +1262,7 @@ int sphx_rcll_grad_normalized_device(sphx_context* ctx, const sphx_grid_desc* gr
     w.gh = h;
     w.galpha = 15.0 / (7.0 * pi_ * h * h);  // make_kernel (kernel.hpp:17-29), dim 2
     NvtxRange nvtx_grad("sphx.pack+grad");
-    ctx->launches += launch_win2(w, true, ctx->stream);
+    ctx->launches += launch_win2(w, true, ctx->stream, ctx->timing ? ctx->ev[1] : nullptr);
     CKL();
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], ctx->stream));
     return SPHX_OK;

@@ -1012,8 +1012,9 @@ void launch_sweep_bt(const Win2Args& a, cudaStream_t st) {
 int64_t win2_tiles(int64_t nrows) { return (nrows + w2_bt() - 1) / w2_bt(); }
 size_t win2_desc_bytes(int64_t nrows) { return sizeof(W2Desc) * (size_t)win2_tiles(nrows); }
 
-// pack + sweep (grad: pack + fused gradient); returns the number of kernels launched
-int launch_win2(const Win2Args& args, bool grad, cudaStream_t st) {
+// pack + sweep (grad: pack + fused gradient); returns the number of kernels launched.
+// mid: an event recorded between the two (timing breakdown only), or null.
+int launch_win2(const Win2Args& args, bool grad, cudaStream_t st, cudaEvent_t mid) {
   Win2Args a = args;
   a.bt = w2_bt();
   a.wcap = a.bt == 256 ? W2Cfg<256>::WCap : W2Cfg<128>::WCap;
@@ -1025,6 +1026,7 @@ int launch_win2(const Win2Args& args, bool grad, cudaStream_t st) {
   const int64_t ntiles = (a.nrows + a.bt - 1) / a.bt;
   const int ntb = (int)((ntiles + 7) / 8);
   k_w2_pack<<<(unsigned)(ntb + ncb + nbr), 256, 0, st>>>(a, ntb, ncb);
+  if (mid) cudaEventRecord(mid, st);
   if (grad) {
     if (a.bt == 256) launch_sweep_bt<256, true>(a, st);
     else launch_sweep_bt<128, true>(a, st);
