@@ -154,7 +154,7 @@ struct sphx_context {
   // device time step: stress (sigma, tau, eps), rates, displacement, max |dx|, status
   Buf s_stress, s_rates, s_dx, s_flags;
   // windowed 2-D FP16 RCLL: CSR-order binary16 x/y pairs, cell x, ids, run lists
-  Buf w_xy, w_u, w_id, w_run, w_desc;
+  Buf w_xy, w_u, w_id, w_run, w_desc, w_cb, w_self;
   // pinned staging for pageable host buffers (two chunks) and their events
   void* h_stage = nullptr;
   cudaEvent_t h_ev[2] = {nullptr, nullptr};
@@ -459,6 +459,8 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
       }
       TRY(ctx->w_run.ensure(32 * (size_t)C));
       TRY(ctx->w_desc.ensure(win2_desc_bytes(nrows)));
+      TRY(ctx->w_cb.ensure(16 * (size_t)C));
+      TRY(ctx->w_self.ensure(4 * (size_t)n));
       SweepArgs& a = *out;
       a.g = grid_consts(g);
       a.c = pc;
@@ -535,6 +537,8 @@ Win2Args win2_args(sphx_context* ctx, const SweepArgs& a) {
   w.wid = ctx->w_id.as<int32_t>();
   w.wrun = ctx->w_run.as<uint8_t>();
   w.desc = ctx->w_desc.p;
+  w.wcb = ctx->w_cb.as<int4>();
+  w.wself = ctx->w_self.as<int32_t>();
   return w;
 }
 
@@ -776,7 +780,7 @@ void sphx_destroy(sphx_context* ctx) {
                 &ctx->b_out_start, &ctx->b_out_items, &ctx->b_rel[0], &ctx->b_rel[1],
                 &ctx->b_rel[2], &ctx->b_cell[0], &ctx->b_cell[1], &ctx->b_cell[2],
                 &ctx->s_stress, &ctx->s_rates, &ctx->s_dx, &ctx->s_flags,
-                &ctx->w_xy, &ctx->w_u, &ctx->w_id, &ctx->w_run, &ctx->w_desc};
+                &ctx->w_xy, &ctx->w_u, &ctx->w_id, &ctx->w_run, &ctx->w_desc, &ctx->w_cb, &ctx->w_self};
   for (Buf* b : all) b->release();
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);

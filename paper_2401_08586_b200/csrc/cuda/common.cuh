@@ -86,6 +86,9 @@ struct Win2Args {
   __half* wu;                 // [n + 16] CSR cell x of each record (binary16)
   int32_t* wid;               // [n + 16] candidate ids (CSR order)
   uint8_t* wrun;              // [C][32] run lists: positions of each x-triple in id order
+  int32_t* wself;             // [n] CSR position of each particle (the inverse of items)
+  int4* wcb;                  // [C] CSR boundaries of each x-triple: L | C | R | end (x = -1:
+                              //     the triple wraps a periodic x axis)
   void* desc;                 // [tiles] W2Desc: each tile's bands and window rows (pack -> sweep)
   int bt, wcap, cscap, runcap;  // the sweep's tile size and shared-memory capacities
   // fused NNPS -> grad_normalized (gradient.cpp:44-82): no table, g per particle

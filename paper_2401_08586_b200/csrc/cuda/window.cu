@@ -51,6 +51,7 @@
 
 #include <climits>
 #include <cstdlib>
+#include <type_traits>
 #include <utility>
 
 #include "common.cuh"
@@ -255,7 +256,15 @@ struct W2Smem {
 // positions; tiles without a window). Positions keep their parity in both, so
 // pair p/2 is the same record pair.
 struct SmemSrc {  // 32-bit shared addresses of the window's arrays
+  static constexpr int kAlign = 2;  // positions per pair load
   uint32_t xy, u, id;
+  __device__ __forceinline__ void quad(int q, uint2 (&v)[4], unsigned (&w)[4]) const {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      v[t] = pair(q + t);
+      w[t] = upair(q + t);
+    }
+  }
   __device__ __forceinline__ uint2 pair(int q) const {
     uint2 v;
     asm("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(xy + 8u * (uint32_t)q));
@@ -273,11 +282,22 @@ struct SmemSrc {  // 32-bit shared addresses of the window's arrays
   }
 };
 struct GlobSrc {
+  static constexpr int kAlign = 8;  // positions per 4-pair vector load
   const uint2* xy;
   const unsigned* u;
   const int* id;
-  __device__ __forceinline__ uint2 pair(int q) const { return __ldg(xy + q); }
-  __device__ __forceinline__ unsigned upair(int q) const { return __ldg(u + q); }
+  // pairs q .. q+3 (q a multiple of 4): one 256-bit and one 128-bit load
+  __device__ __forceinline__ void quad(int q, uint2 (&v)[4], unsigned (&w)[4]) const {
+    asm("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(v[0].x), "=r"(v[0].y), "=r"(v[1].x), "=r"(v[1].y), "=r"(v[2].x), "=r"(v[2].y),
+          "=r"(v[3].x), "=r"(v[3].y)
+        : "l"(xy + q));
+    const uint4 t = __ldg(reinterpret_cast<const uint4*>(u + q));
+    w[0] = t.x;
+    w[1] = t.y;
+    w[2] = t.z;
+    w[3] = t.w;
+  }
   __device__ __forceinline__ int ident(int p) const { return __ldg(id + p); }
 };
 
@@ -343,10 +363,15 @@ __device__ __forceinline__ Seg seg_glob(const Win2Args& a, int cx, int cy, int s
     y = (y + ny) % ny;
   }
   const int64_t row = (int64_t)y * nx;
-  g.pL = __ldg(a.start + row + max(cx - 1, 0));
-  g.pC = __ldg(a.start + row + cx);
-  g.pR = __ldg(a.start + row + cx + 1);
-  g.pE = __ldg(a.start + row + min(cx + 1, nx - 1) + 1);
+  const int4 b = __ldg(a.wcb + row + cx);  // the pack's boundaries of the triple
+  if (b.x < 0) {
+    ok = false;
+    return g;
+  }
+  g.pL = b.x;
+  g.pC = b.y;
+  g.pR = b.z;
+  g.pE = b.w;
   g.r = (int)(row + cx);  // the centre cell
   return g;
 }
@@ -508,7 +533,9 @@ __global__ void __launch_bounds__(256) k_w2_pack(Win2Args a, int ntb, int ncb) {
       for (int s = m1; s < m2; ++s) a.wu[s] = hx;
       const int s0 = x > 0 ? sst[tid] : m1;
       const int e = x + 1 < nx ? sst[tid + 3] : m2;
-      if (e - s0 <= kSegMax && !(a.g.wrap[0] && (x == 0 || x == nx - 1))) {
+      const bool wraps = a.g.wrap[0] && (x == 0 || x == nx - 1);
+      a.wcb[v] = wraps ? make_int4(-1, -1, -1, -1) : make_int4(s0, m1, m2, e);
+      if (e - s0 <= kSegMax && !wraps) {
         int iL = s0, iC = m1, iR = m2;
         int vL = iL < m1 ? ids[iL] : INT_MAX;
         int vC = iC < m2 ? ids[iC] : INT_MAX;
@@ -562,6 +589,7 @@ __global__ void __launch_bounds__(256) k_w2_pack(Win2Args a, int ntb, int ncb) {
     a.wxy[4 * p + h] = __double2half(rx[q]);
     a.wxy[4 * p + 2 + h] = __double2half(ry[q]);
     a.wid[s] = id[q];
+    a.wself[id[q]] = s;
   }
   pdl_trigger();
 }
@@ -813,12 +841,14 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
     if (!ok) slow = true;
     return g;
   };
+  const int selfcsr = valid ? __ldg(a.wself + i) : 0;
   auto phase_a = [&](const auto& src) {  // every lane: warp-uniform loops
     int tot = 0;
 #pragma unroll
     for (int s = 0; s < 3; ++s) {
       const Seg g = seg(s);
-      const int p0 = g.pL & ~1;
+      constexpr int kA = std::decay_t<decltype(src)>::kAlign;
+      const int p0 = g.pL & ~(kA - 1);
       if (g.pE - p0 > kSegMax) slow = true;
       // pairs of this lane; the loop runs the warp's maximum (lanes past their
       // segment test the records that follow it, masked out below)
@@ -834,11 +864,7 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
         if (t0 >= npmax) break;
         uint2 xy[4];
         unsigned u2[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          xy[t] = src.pair(q0 + t0 + t);
-          u2[t] = src.upair(q0 + t0 + t);
-        }
+        src.quad(q0 + t0, xy, u2);
 #pragma unroll
         for (int t = 0; t < 4; ++t)
           pair_test(xy[t].x, xy[t].y, u2[t], rx2, ry2, ut2, hhx, hhy, hc2, ccy, s != 1, thr2,
@@ -846,14 +872,10 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
       }
       H &= above(g.pL - p0) & ~above(g.pE - p0);  // bit q = position p0 + q
       if (s == 1 && !slow) {
-        // the target's own record: its id among the (ascending) ids of its cell
-        int lo = g.pC, hi = g.pR;
-        while (lo < hi) {
-          const int m = (lo + hi) >> 1;
-          if (src.ident(m) < i) lo = m + 1;
-          else hi = m;
-        }
-        if (lo < g.pR && src.ident(lo) == i) H &= ~(1u << (lo - p0));
+        // the target's own record (its CSR position from the pack), which must
+        // lie in its centre cell
+        const int sp = fast ? S.d.rbase[g.r] + (selfcsr - S.d.ra8[g.r]) : selfcsr;
+        if (sp >= g.pC && sp < g.pR) H &= ~(1u << (sp - p0));
         else slow = true;  // RelCoords cell is not the CSR cell (a stale grid)
       }
       S.hw[s][tid] = H;
@@ -891,7 +913,8 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
       const int pL = g.pL, len = g.pE - g.pL;
       const int lmax = __reduce_max_sync(0xffffffffu, len);
       if (lmax == 0) continue;
-      const unsigned hrel = H >> (pL & 1);  // bit o = position pL + o
+      constexpr int kA = std::decay_t<decltype(src)>::kAlign;
+      const unsigned hrel = H >> (pL & (kA - 1));  // bit o = position pL + o
       uint4 w[2];
       if (fast) {
         const uint4* rl = &S.run[2 * (H ? G.run0(g.r) + cx - S.d.bx[b][0] : 0)];
