@@ -1009,14 +1009,10 @@ void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t 
   cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
-// rows per tile: SPHX_W2BT=128|256 (default 128)
+// rows per tile: SPHX_W2BT=128|256 (default 128; read per call)
 int w2_bt() {
-  static int bt = 0;
-  if (!bt) {
-    const char* e = std::getenv("SPHX_W2BT");
-    bt = (e && std::atoi(e) == 256) ? 256 : 128;
-  }
-  return bt;
+  const char* e = std::getenv("SPHX_W2BT");
+  return (e && std::atoi(e) == 256) ? 256 : 128;
 }
 
 template <int BT, bool GRAD>

@@ -89,3 +89,40 @@ def test_gradient_rejects_non_fp16(ctx):
     rel, cell, _, start, items = ctx.build_rel_coords(g, x)
     with pytest.raises(ValueError):
         ctx.rcll_grad_normalized(g, rel, cell, items, start, 0, x, x[0], 0.12)
+
+
+@pytest.mark.parametrize("order", ["shuffled", "reversed"])
+def test_gradient_2d_particle_orders(ctx, order):
+    """Incoherent id orders: the windowed gradient's tiles without a window."""
+    x = O.Oracle().lattice(2, 0.01, 0.3, 4)
+    rs = np.random.default_rng(11)
+    perm = rs.permutation(len(x[0])) if order == "shuffled" else np.arange(len(x[0]))[::-1]
+    x = [np.ascontiguousarray(a[perm]) for a in x]
+    _check(ctx, x, 0.024, 0.012)
+
+
+def test_gradient_2d_dense_cluster(ctx):
+    """A dense blob: segments beyond 32 records and tiles whose rows do not fit the
+    shared-memory row buffer (the selection walk)."""
+    rs = np.random.default_rng(6)
+    x = np.concatenate([0.45 + 0.012 * rs.standard_normal((2, 2500)), rs.random((2, 500))], axis=1)
+    x = [np.ascontiguousarray(a) for a in np.clip(x, 0.0, 1.0 - 1e-12)]
+    _check(ctx, x, 0.048, 0.024)
+
+
+def test_gradient_2d_matches_encode_path(ctx):
+    """The windowed fused gradient equals the encode + k_r16_grad one (SPHX_W2=0)."""
+    import os
+
+    import paper_2401_08586_b200 as P
+    x = O.Oracle().lattice(2, 1.0 / 317, 0.3, 8)
+    g = P.grid_init(2, (0, 0, 0), (1, 1, 1), 2.4 / 317)
+    rel, cell, _, start, items = ctx.build_rel_coords(g, x)
+    f = np.sin(9.0 * x[0]) + x[1]
+    a = ctx.rcll_grad_normalized(g, rel, cell, items, start, 2, x, f, 1.2 / 317)
+    os.environ["SPHX_W2"] = "0"
+    try:
+        b = ctx.rcll_grad_normalized(g, rel, cell, items, start, 2, x, f, 1.2 / 317)
+    finally:
+        del os.environ["SPHX_W2"]
+    assert all(np.array_equal(a[0][k], b[0][k]) for k in range(2)) and a[1] == b[1]

@@ -20,15 +20,18 @@ from golden_cases import load_cases, load_configs
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True)
-def windowed():
-    old = os.environ.get("SPHX_W2")
+@pytest.fixture(autouse=True, params=["128", "256"], ids=["bt128", "bt256"])
+def windowed(request):
+    """Both tile sizes (SPHX_W2BT) of the windowed path."""
+    old = {k: os.environ.get(k) for k in ("SPHX_W2", "SPHX_W2BT")}
     os.environ["SPHX_W2"] = "1"
+    os.environ["SPHX_W2BT"] = request.param
     yield
-    if old is None:
-        del os.environ["SPHX_W2"]
-    else:
-        os.environ["SPHX_W2"] = old
+    for k, v in old.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
 
 
 @pytest.fixture(scope="module")
