@@ -443,7 +443,7 @@ int run_prepare(sphx_context* ctx, int mode, const sphx_grid_desc& g, int64_t n6
     return SPHX_OK;
   }
   const int64_t C = mode == MODE_ALL ? 0 : cell_total(g);
-  if (allow_window && g.dim == 2 && prec == SPHX_FP16 && mode == MODE_RCLL && !sel.ids &&
+  if (allow_window && g.dim == 2 && prec == SPHX_FP16 && mode == MODE_RCLL &&
       g.counts[0] <= 2048 && win2_enabled()) {
     const PrecConsts pc = make_consts(mode, prec, g, h);
     if (pc.h_thr != 0) {  // (thr == 0: no pair can hit; the generic path handles it)
@@ -537,6 +537,7 @@ Win2Args win2_args(sphx_context* ctx, const SweepArgs& a) {
   w.wid = ctx->w_id.as<int32_t>();
   w.wrun = ctx->w_run.as<uint8_t>();
   w.desc = ctx->w_desc.p;
+  w.ids = a.ids;
   w.wcb = ctx->w_cb.as<int4>();
   w.wself = ctx->w_self.as<int32_t>();
   return w;

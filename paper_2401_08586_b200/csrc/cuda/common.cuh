@@ -81,10 +81,11 @@ struct Win2Args {
   const double* rel[2];       // RelCoords::rel[k] (particle order)
   const int32_t* cellk[2];    // RelCoords::cell[k]
   const int32_t* items;       // CellGrid::items (CSR)
-  const int32_t* start;       // CellGrid::cell_start [C+1]
+ const int32_t* start;       // CellGrid::cell_start [C+1]
   __half* wxy;                // [n + 16] pair-interleaved binary16 x / y (CSR order)
   __half* wu;                 // [n + 16] CSR cell x of each record (binary16)
-  int32_t* wid;               // [n + 16] candidate ids (CSR order)
+  int32_t* wid;               // [n + 16] candidate ids (CSR order; global ids of a slab)
+  const int32_t* ids;         // output id of local particle j (null: j) -- a slab's global ids
   uint8_t* wrun;              // [C][32] run lists: positions of each x-triple in id order
   int32_t* wself;             // [n] CSR position of each particle (the inverse of items)
   int4* wcb;                  // [C] CSR boundaries of each x-triple: L | C | R | end (x = -1:

@@ -521,9 +521,17 @@ __global__ void __launch_bounds__(256) k_w2_pack(Win2Args a, int ntb, int ncb) {
     const int lo = sst[0], hi = sst[256 + 2];
     const bool staged = hi - lo <= kSpan;
     if (staged)
-      for (int e = tid; e < hi - lo; e += 256) sid[e] = __ldg(a.items + lo + e);
+      for (int e = tid; e < hi - lo; e += 256) {
+        const int j = __ldg(a.items + lo + e);
+        sid[e] = a.ids ? __ldg(a.ids + j) : j;  // merged by output id
+      }
     __syncthreads();
-    const int* ids = staged ? sid - lo : a.items;
+    const int* sids = sid - lo;
+    auto key = [&](int p) {  // the output id at CSR position p
+      if (staged) return sids[p];
+      const int j = __ldg(a.items + p);
+      return a.ids ? __ldg(a.ids + j) : j;
+    };
     const int64_t v = v0 + tid;
     const int nx = a.g.counts[0];
     const int x = (int)(v % nx);
@@ -537,9 +545,9 @@ __global__ void __launch_bounds__(256) k_w2_pack(Win2Args a, int ntb, int ncb) {
       a.wcb[v] = wraps ? make_int4(-1, -1, -1, -1) : make_int4(s0, m1, m2, e);
       if (e - s0 <= kSegMax && !wraps) {
         int iL = s0, iC = m1, iR = m2;
-        int vL = iL < m1 ? ids[iL] : INT_MAX;
-        int vC = iC < m2 ? ids[iC] : INT_MAX;
-        int vR = iR < e ? ids[iR] : INT_MAX;
+        int vL = iL < m1 ? key(iL) : INT_MAX;
+        int vC = iC < m2 ? key(iC) : INT_MAX;
+        int vR = iR < e ? key(iR) : INT_MAX;
         unsigned w[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) w[q] = 0xFFFFFFFFu;
@@ -553,7 +561,7 @@ __global__ void __launch_bounds__(256) k_w2_pack(Win2Args a, int ntb, int ncb) {
           else if (tc) ++iC;
           else ++iR;
           const int nxt = pos + 1;
-          const int nv = (tl ? nxt < m1 : (tc ? nxt < m2 : nxt < e)) ? ids[nxt] : INT_MAX;
+          const int nv = (tl ? nxt < m1 : (tc ? nxt < m2 : nxt < e)) ? key(nxt) : INT_MAX;
           vL = tl ? nv : vL;
           vC = tc ? nv : vC;
           vR = (!tl && !tc) ? nv : vR;
@@ -571,10 +579,12 @@ __global__ void __launch_bounds__(256) k_w2_pack(Win2Args a, int ntb, int ncb) {
   int id[kPackR];
   double rx[kPackR], ry[kPackR];
   const int s0 = (blockIdx.x - ntb - ncb) * 256 * kPackR + tid;
+  // the CSR's records (a slab's arrays have spare capacity past them)
+  const int nrec = __ldg(a.start + (int64_t)a.g.counts[0] * a.g.counts[1]);
 #pragma unroll
   for (int q = 0; q < kPackR; ++q) {
     const int s = s0 + 256 * q;
-    id[q] = s < a.n ? __ldg(a.items + s) : 0;
+    id[q] = s < nrec ? __ldg(a.items + s) : 0;
   }
 #pragma unroll
   for (int q = 0; q < kPackR; ++q) {
@@ -584,11 +594,11 @@ __global__ void __launch_bounds__(256) k_w2_pack(Win2Args a, int ntb, int ncb) {
 #pragma unroll
   for (int q = 0; q < kPackR; ++q) {
     const int s = s0 + 256 * q;
-    if (s >= a.n) break;
+    if (s >= nrec) break;
     const int p = s >> 1, h = s & 1;
     a.wxy[4 * p + h] = __double2half(rx[q]);
     a.wxy[4 * p + 2 + h] = __double2half(ry[q]);
-    a.wid[s] = id[q];
+    a.wid[s] = a.ids ? __ldg(a.ids + id[q]) : id[q];
     a.wself[id[q]] = s;
   }
   pdl_trigger();
@@ -610,6 +620,7 @@ __device__ int w2_slow_row(const Win2Args& a, int i, int cxi, int cyi, __half rx
   const int nx = a.g.counts[0], ny = a.g.counts[1];
   const __half hhx = hb(a.c.h_hh[0]), hhy = hb(a.c.h_hh[1]);
   const __half thr = hb(a.c.h_thr);
+  const int gi = a.ids ? __ldg(a.ids + i) : i;  // the target's output id
   int k = 0;
   for (int oy = -1; oy <= 1; ++oy) {
     int cy = cyi + oy;
@@ -629,7 +640,7 @@ __device__ int w2_slow_row(const Win2Args& a, int i, int cxi, int cyi, __half rx
       const __half ccx = cc_half(a.c.h_cc[0], ox);  // r16(dc*hc), dc = -ox
       for (int s = b; s < e; ++s) {
         const int j = __ldg(a.wid + s);
-        if (j == i) continue;
+        if (j == gi) continue;
         const __half dx = __hadd_rn(__hmul_rn(__hsub_rn(rx, w2_x(a, s)), hhx), ccx);
         const __half dy = __hadd_rn(__hmul_rn(__hsub_rn(ry, w2_y(a, s)), hhy), ccy);
         const __half acc = __hadd_rn(__hmul_rn(dx, dx), __hmul_rn(dy, dy));
