@@ -19,7 +19,8 @@
  *                                                                   cell_grid.hpp:120, cell_grid.cpp:114-133
  *   sphx_rebuild_members <- void CellGrid::rebuild_members(const RelCoords&)
  *                                                                   cell_grid.hpp:89, cell_grid.cpp:86-108
- *   sphx_table_copy      <- (ownership hand-off of the returned NeighborTable, nnps.hpp:16-26)
+ *   sphx_table_copy / sphx_table_stream
+ *                        <- (ownership hand-off of the returned NeighborTable, nnps.hpp:16-26)
  *   sphx_update_relative(_device)
  *                        <- void update_relative(RelCoords&, size_t i, const std::array<double,3>&,
  *                                                const CellGrid&, Precision) for all i
@@ -132,6 +133,15 @@ int sphx_all_list(sphx_context* ctx, int32_t dim, int64_t n, const double* const
 /* Copy the last table computed on this context to host buffers: offsets[n+1],
  * items[total]. Either pointer may be NULL. */
 int sphx_table_copy(sphx_context* ctx, int64_t* offsets, int32_t* items);
+
+/* Stream the last table to a consumer that builds its own container (the
+ * drop-in's std::vector, filled by insertion instead of a zero-fill plus a copy):
+ * sink(user, part, data, bytes) is called in order for part 0 (offsets, int64)
+ * and then part 1 (items, int32) with consecutive chunks of whole elements; the
+ * next chunk's DMA overlaps the sink. A nonzero sink result stops the copy with
+ * SPHX_ERR_RUNTIME. (Same hand-off as sphx_table_copy, nnps.hpp:16-26.) */
+typedef int (*sphx_table_sink)(void* user, int32_t part, const void* data, int64_t bytes);
+int sphx_table_stream(sphx_context* ctx, sphx_table_sink sink, void* user);
 
 /* CellGrid::rebin(ps): cell_of[n], cell_start[cell_total+1], items[n]. A particle
  * outside the grid -> SPHX_ERR_OUT_OF_RANGE "particle <i> lies outside the grid"

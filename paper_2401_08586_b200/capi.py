@@ -45,6 +45,8 @@ class GridDesc(C.Structure):
 
 
 _lib = None
+# int sink(void* user, int32_t part, const void* data, int64_t bytes)  (sphx_cuda.h)
+TABLE_SINK = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.c_void_p, C.c_int64)
 
 
 def lib():
@@ -71,6 +73,7 @@ def lib():
                                           C.POINTER(i64)]),
         "sphx_all_list": (C.c_int, [vp, i32, i64, p3, dbl, i32, C.POINTER(i64)]),
         "sphx_table_copy": (C.c_int, [vp, vp, vp]),
+        "sphx_table_stream": (C.c_int, [vp, TABLE_SINK, vp]),
         "sphx_rebin": (C.c_int, [vp, G, i64, p3, vp, vp, vp]),
         "sphx_build_rel_coords": (C.c_int, [vp, G, i64, p3, p3, p3, vp, vp, vp]),
         "sphx_rebuild_members": (C.c_int, [vp, G, i64, p3, vp, vp, vp]),
@@ -117,7 +120,7 @@ def lib():
 
 EXPORTED = ("sphx_last_error", "sphx_grid_init", "sphx_create", "sphx_destroy",
             "sphx_set_stream", "sphx_launch_count", "sphx_rcll", "sphx_cell_link_list",
-            "sphx_all_list", "sphx_table_copy", "sphx_rebin", "sphx_build_rel_coords",
+            "sphx_all_list", "sphx_table_copy", "sphx_table_stream", "sphx_rebin", "sphx_build_rel_coords",
             "sphx_rebuild_members", "sphx_rcll_device", "sphx_cell_link_list_device",
             "sphx_build_rel_coords_device", "sphx_rebin_device", "sphx_enable_timing",
             "sphx_last_timing", "sphx_build_lattice", "sphx_build_random_uniform",
@@ -274,6 +277,17 @@ class Context:
         items = np.empty(max(total, 1), np.int32)
         check(lib().sphx_table_copy(self.h, off.ctypes.data, items.ctypes.data))
         return off, items[:total]
+
+    def table_stream(self, sink):
+        """sphx_table_stream: sink(part, bytes) gets the offsets (part 0) and then
+        the items (part 1) chunk by chunk; a falsy/raising sink stops the copy."""
+        def cb(_user, part, data, nbytes):
+            try:
+                return 0 if sink(part, C.string_at(data, nbytes)) is not False else 1
+            except Exception:  # noqa: BLE001 - reported through the C ABI
+                return 1
+        fn = TABLE_SINK(cb)
+        check(lib().sphx_table_stream(self.h, fn, None))
 
     def rcll(self, grid: GridDesc, rel, cell, items, cell_start, prec: int):
         rel = [_c64(a) for a in rel]

@@ -28,39 +28,54 @@ int32_t prec_code(Precision p) {
   return p == Precision::fp64 ? SPHX_FP64 : (p == Precision::fp32 ? SPHX_FP32 : SPHX_FP16);
 }
 
-// Sizes a fresh output vector. A large table's first touch is the drop-in's
-// biggest host cost (4 KB page faults + zero-fill: 28 ms for C2's 78 MB,
-// measured): its storage is asked for transparent huge pages and faulted in by
-// several threads before the (single-threaded) value-initialisation.
+// Reserves a fresh output vector's storage. A large table's first touch is the
+// drop-in's biggest host cost (4 KB page faults + zero-fill: 28 ms for C2's
+// 78 MB, measured): the storage is asked for transparent huge pages and faulted
+// in by several threads; the elements are then appended straight from the DMA
+// stage (sphx_table_stream), so the vector is never zero-filled.
 template <class T>
-void fresh_vector(std::vector<T>& v, std::size_t n) {
+void fresh_storage(std::vector<T>& v, std::size_t n) {
   constexpr std::size_t kBig = std::size_t(8) << 20, kHuge = std::size_t(2) << 20;
   const std::size_t bytes = n * sizeof(T);
-  if (bytes >= kBig) {
-    v.reserve(n);
-    const auto base = reinterpret_cast<std::uintptr_t>(v.data());
-    const std::uintptr_t a = (base + kHuge - 1) & ~(kHuge - 1);
-    if (a < base + bytes) madvise(reinterpret_cast<void*>(a), base + bytes - a, MADV_HUGEPAGE);
-    // fault the pages in (zero bytes into the vector's own, not yet used storage)
-    constexpr int kT = 8;
-    std::thread th[kT - 1];
-    auto part = [&](int k) {
-      volatile char* p = reinterpret_cast<char*>(v.data());
-      for (std::size_t o = bytes * k / kT; o < bytes * (k + 1) / kT; o += 4096) p[o] = 0;
-    };
-    for (int k = 1; k < kT; ++k) th[k - 1] = std::thread(part, k);
-    part(0);
-    for (auto& t : th) t.join();
+  v.clear();
+  v.reserve(n);
+  if (bytes < kBig) return;
+  const auto base = reinterpret_cast<std::uintptr_t>(v.data());
+  const std::uintptr_t a = (base + kHuge - 1) & ~(kHuge - 1);
+  if (a < base + bytes) madvise(reinterpret_cast<void*>(a), base + bytes - a, MADV_HUGEPAGE);
+  // fault the pages in (zero bytes into the vector's own, not yet used storage)
+  constexpr int kT = 8;
+  std::thread th[kT - 1];
+  auto part = [&](int k) {
+    volatile char* p = reinterpret_cast<char*>(v.data());
+    for (std::size_t o = bytes * k / kT; o < bytes * (k + 1) / kT; o += 4096) p[o] = 0;
+  };
+  for (int k = 1; k < kT; ++k) th[k - 1] = std::thread(part, k);
+  part(0);
+  for (auto& t : th) t.join();
+}
+
+// sphx_table_stream sink: appends each chunk to offsets (part 0) or items (part 1)
+int append_chunk(void* user, std::int32_t part, const void* data, std::int64_t bytes) {
+  auto& t = *static_cast<NeighborTable*>(user);
+  if (part == 0) {
+    const auto* p = static_cast<const std::int64_t*>(data);
+    t.offsets.insert(t.offsets.end(), p, p + bytes / std::int64_t(sizeof(std::int64_t)));
+  } else {
+    const auto* p = static_cast<const std::int32_t*>(data);
+    t.items.insert(t.items.end(), p, p + bytes / std::int64_t(sizeof(std::int32_t)));
   }
-  v.resize(n);
+  return 0;
 }
 
 NeighborTable take_table(sphx_context* ctx, std::size_t n, std::int64_t total, double radius) {
   NeighborTable t;
   t.radius = radius;
-  fresh_vector(t.offsets, n + 1);
-  fresh_vector(t.items, static_cast<std::size_t>(total));
-  cuda::check(sphx_table_copy(ctx, t.offsets.data(), t.items.empty() ? nullptr : t.items.data()));
+  fresh_storage(t.offsets, n + 1);
+  fresh_storage(t.items, static_cast<std::size_t>(total));
+  cuda::check(sphx_table_stream(ctx, append_chunk, &t));
+  if (t.offsets.size() != n + 1 || t.items.size() != static_cast<std::size_t>(total))
+    throw std::runtime_error("table hand-off is incomplete");
   return t;
 }
 

@@ -94,6 +94,33 @@ def test_config_golden_hashes(ctx, P, name):
         assert f"{O.fnv_hash(*t):016x}" == want["hash"], f"cll {prec} hash"
 
 
+def test_table_stream_matches_golden_c2(ctx, P):
+    """sphx_table_stream (the drop-in's hand-off, sphx_cuda.h) delivers the offsets
+    then the items in whole-element chunks (C2's 78 MB table: several 16 MB
+    stage chunks) that concatenate to the golden table; a failing sink stops the
+    copy with an error, and the table stays available afterwards."""
+    c, x, h = _config_inputs("C2")
+    g = P.grid_init(2, (0, 0, 0), (1, 1, 1), 2.0 * h)
+    rel, cell, cell_of, start, items = ctx.build_rel_coords(g, x)
+    off, it = ctx.rcll(g, rel, cell, items, start, PREC["fp16"])
+    parts, seen = {0: [], 1: []}, []
+    ctx.table_stream(lambda part, b: (seen.append(part), parts[part].append(b)) and None)
+    assert seen == sorted(seen) and seen.count(1) > 1
+    assert all(len(b) % 8 == 0 for b in parts[0]) and all(len(b) % 4 == 0 for b in parts[1])
+    s_off = np.frombuffer(b"".join(parts[0]), np.int64)
+    s_it = np.frombuffer(b"".join(parts[1]), np.int32)
+    assert np.array_equal(s_off, off) and np.array_equal(s_it, it)
+    want = c["tables"]["rcll_fp16"]
+    assert f"{O.fnv_hash(s_off, s_it):016x}" == want["hash"]
+    calls = []
+    with pytest.raises(RuntimeError, match="sink"):
+        ctx.table_stream(lambda part, b: calls.append(part) or False)
+    assert calls == [0]
+    again = []
+    ctx.table_stream(lambda part, b: again.append(len(b)) and None)
+    assert sum(again) == 8 * len(off) + 4 * len(it)
+
+
 def test_binning_matches_oracle_c2(ctx, P):
     c, x, h = _config_inputs("C2")
     orc = O.Oracle()
