@@ -718,7 +718,9 @@ def bench_grad(args, w, ctx, stream, grid, n, C, xd, rel, cell, items, start, lo
                    "n_particles": n, "pairs_not_materialised": tab.total,
                    "l2": "flushed between timed steps"},
         "parity": {"bit_exact_vs_oracle": bool(exact), "degenerate": int(deg.item())},
-        "roofline": {"bound": "hbm", "kernel": "k_encode_rows + k_r16_grad",
+        "roofline": {"bound": "hbm",
+                     "kernel": ("k_w2_pack + k_w2<128, GRAD> (windowed rows walked into FP64 sums)"
+                                if dim == 2 else "k_encode_rows + k_r16_grad"),
                      "achieved": (b_in + b_out) / t / 1e9, "peak": peak, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": (b_in + b_out) / t / 1e9 / peak,
                      "algorithmic_bytes": b_in + b_out,

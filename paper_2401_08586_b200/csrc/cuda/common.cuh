@@ -123,6 +123,18 @@ struct SlabArgs {
 // Look-back words carry flag and value in one 64-bit word, so relaxed gpu-scope
 // accesses suffice. (An acquire load would compile to CCTL.IVALL -- an L1
 // invalidation per spin iteration that evicts every warp's cached candidates.)
+// RN(r / h) for a launch-constant h from y = RN(1/h) (__drcp_rn): two FMA
+// residual corrections. After the first, q is within one ulp of r/h, so the
+// second is Markstein's correctly rounded step (Handbook of Floating-Point
+// Arithmetic, Markstein's theorem: y within half an ulp of 1/h, q within one ulp,
+// the residual r - hq exact by FMA => RN(q + (r - hq) y) = RN(r/h)): the bits of
+// __ddiv_rn(r, h) for normal operands, in five FP64 ops instead of its ~20.
+__device__ __forceinline__ double div_by(double r, double h, double y) {
+  double q = __dmul_rn(r, y);
+  q = __fma_rn(__fma_rn(-q, h, r), y, q);
+  return __fma_rn(__fma_rn(-q, h, r), y, q);
+}
+
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");

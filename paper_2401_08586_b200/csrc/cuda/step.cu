@@ -34,7 +34,8 @@ __device__ __forceinline__ double dwdr(double R, double alpha) {
 
 // kernel_grad(dx, kp) for dx = x_i - x_j
 template <int D>
-__device__ __forceinline__ void kgrad(const double (&dx)[3], double h, double alpha, double (&gw)[3]) {
+__device__ __forceinline__ void kgrad(const double (&dx)[3], double h, double ih, double alpha,
+                                      double (&gw)[3]) {
   double r2 = 0.0;
 #pragma unroll
   for (int k = 0; k < D; ++k) r2 = __dadd_rn(r2, __dmul_rn(dx[k], dx[k]));
@@ -42,7 +43,7 @@ __device__ __forceinline__ void kgrad(const double (&dx)[3], double h, double al
 #pragma unroll
   for (int k = 0; k < 3; ++k) gw[k] = 0.0;
   if (r == 0.0) return;
-  const double R = __ddiv_rn(r, h);
+  const double R = div_by(r, h, ih);  // ih = RN(1/h)
   const double sc = __ddiv_rn(dwdr(R, alpha), __dmul_rn(h, r));
 #pragma unroll
   for (int k = 0; k < D; ++k) gw[k] = __dmul_rn(sc, dx[k]);
@@ -63,6 +64,7 @@ template <int D>
 __global__ void __launch_bounds__(128) k_stress(StepArgs a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
+  const double ih = __drcp_rn(a.h);
   double xi[3], vi[3];
 #pragma unroll
   for (int k = 0; k < D; ++k) {
@@ -76,7 +78,7 @@ __global__ void __launch_bounds__(128) k_stress(StepArgs a) {
     double dx[3] = {0.0, 0.0, 0.0}, gw[3];
 #pragma unroll
     for (int k = 0; k < D; ++k) dx[k] = __dsub_rn(xi[k], __ldg(a.x[k] + j));
-    kgrad<D>(dx, a.h, a.alpha, gw);
+    kgrad<D>(dx, a.h, ih, a.alpha, gw);
 #pragma unroll
     for (int c = 0; c < D; ++c) {  // grad_normalized(v_c): num += (f_j - f_i) gw
       const double df = __dsub_rn(__ldg(a.v[c] + j), vi[c]);
@@ -114,6 +116,7 @@ template <int D>
 __global__ void __launch_bounds__(128) k_rates(StepArgs a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
+  const double ih = __drcp_rn(a.h);
   double xi[3], vi[3], si[6];
 #pragma unroll
   for (int k = 0; k < D; ++k) {
@@ -133,7 +136,7 @@ __global__ void __launch_bounds__(128) k_rates(StepArgs a) {
     double dx[3] = {0.0, 0.0, 0.0}, gw[3];
 #pragma unroll
     for (int k = 0; k < D; ++k) dx[k] = __dsub_rn(xi[k], __ldg(a.x[k] + j));
-    kgrad<D>(dx, a.h, a.alpha, gw);
+    kgrad<D>(dx, a.h, ih, a.alpha, gw);
     const double mj = __ldg(a.m + j);
     double dv_dot = 0.0;  // rhs_density / rhs_energy
 #pragma unroll

@@ -1270,10 +1270,15 @@ __device__ __forceinline__ double kdwdr(double R, double alpha) {
 }
 
 template <int D>
+struct GradTerm {
+  double num[3], den[3], scale[3];
+};
+
+template <int D>
 struct GradAcc {
   double num[3] = {0.0, 0.0, 0.0}, den[3] = {0.0, 0.0, 0.0}, scale[3] = {0.0, 0.0, 0.0};
-  double xi[3], fi;
-  __device__ __forceinline__ void add(const SweepArgs& a, int j) {
+  double xi[3], fi, ih;  // ih = RN(1/h)
+  __device__ __forceinline__ GradTerm<D> term(const SweepArgs& a, int j) const {
     double dx[3], gw[3] = {0.0, 0.0, 0.0}, r2 = 0.0;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
@@ -1282,19 +1287,30 @@ struct GradAcc {
     }
     const double r = __dsqrt_rn(r2);
     if (r != 0.0) {
-      const double R = __ddiv_rn(r, a.gh);
+      const double R = div_by(r, a.gh, ih);
       const double sc = __ddiv_rn(kdwdr(R, a.galpha), __dmul_rn(a.gh, r));
 #pragma unroll
       for (int k = 0; k < D; ++k) gw[k] = __dmul_rn(sc, dx[k]);
     }
     const double df = __dsub_rn(__ldg(a.gf + j), fi);
+    GradTerm<D> t;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      num[k] = __dadd_rn(num[k], __dmul_rn(df, gw[k]));
-      den[k] = __dadd_rn(den[k], __dmul_rn(-dx[k], gw[k]));
-      scale[k] = __dadd_rn(scale[k], fabs(__dmul_rn(dx[k], gw[k])));
+      t.num[k] = __dmul_rn(df, gw[k]);
+      t.den[k] = __dmul_rn(-dx[k], gw[k]);
+      t.scale[k] = fabs(__dmul_rn(dx[k], gw[k]));
+    }
+    return t;
+  }
+  __device__ __forceinline__ void acc(const GradTerm<D>& t) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      num[k] = __dadd_rn(num[k], t.num[k]);
+      den[k] = __dadd_rn(den[k], t.den[k]);
+      scale[k] = __dadd_rn(scale[k], t.scale[k]);
     }
   }
+  __device__ __forceinline__ void add(const SweepArgs& a, int j) { acc(term(a, j)); }
 };
 
 template <int D, int BT, int CAP, int W>
@@ -1335,6 +1351,7 @@ __global__ void __launch_bounds__(BT) k_r16_grad(SweepArgs a) {
 #pragma unroll
     for (int kk = 0; kk < D; ++kk) acc.xi[kk] = __ldg(a.gx[kk] + i);
     acc.fi = __ldg(a.gf + i);
+    acc.ih = __drcp_rn(a.gh);
     if (k <= CAP) {
       // B: the sorted row in this thread's slot, then the gradient over it
       const SharedRow row{(uint32_t)__cvta_generic_to_shared(ROWS) + 4u * (uint32_t)(tid * CAP)};
@@ -1354,7 +1371,13 @@ __global__ void __launch_bounds__(BT) k_r16_grad(SweepArgs a) {
         }
         if (gs > 0 && kk > gs && row.ld(gs) < row.ld(gs - 1)) merge_tail(row, gs, kk);
       });
-      for (int e = 0; e < k; ++e) acc.add(a, row.ld(e));
+      int e = 0;  // two neighbours' terms in flight, summed in row order
+      for (; e + 1 < k; e += 2) {
+        const GradTerm<D> t0 = acc.term(a, row.ld(e)), t1 = acc.term(a, row.ld(e + 1));
+        acc.acc(t0);
+        acc.acc(t1);
+      }
+      if (e < k) acc.add(a, row.ld(e));
     } else {
       // long row: ids in ascending order by repeated minimum search over the hits
       int last = INT_MIN;

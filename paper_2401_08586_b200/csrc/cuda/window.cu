@@ -666,10 +666,15 @@ __device__ __forceinline__ double w2_dwdr(double R, double alpha) {
   }
   return 0.0;
 }
+// One neighbour's contributions to the three sums (the same for (i,j) and (j,i)).
+struct W2Term {
+  double num[2], den[2], scale[2];
+};
+
 struct W2Grad {
   double num[2] = {0.0, 0.0}, den[2] = {0.0, 0.0}, scale[2] = {0.0, 0.0};
-  double xi[2], fi;
-  __device__ __forceinline__ void add(const Win2Args& a, int j) {
+  double xi[2], fi, ih;  // ih = RN(1/h)
+  __device__ __forceinline__ W2Term term(const Win2Args& a, int j) const {
     double dx[2], gw[2] = {0.0, 0.0}, r2 = 0.0;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
@@ -678,19 +683,30 @@ struct W2Grad {
     }
     const double r = __dsqrt_rn(r2);
     if (r != 0.0) {
-      const double R = __ddiv_rn(r, a.gh);
+      const double R = div_by(r, a.gh, ih);
       const double sc = __ddiv_rn(w2_dwdr(R, a.galpha), __dmul_rn(a.gh, r));
 #pragma unroll
       for (int k = 0; k < 2; ++k) gw[k] = __dmul_rn(sc, dx[k]);
     }
     const double df = __dsub_rn(__ldg(a.gf + j), fi);
+    W2Term t;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      num[k] = __dadd_rn(num[k], __dmul_rn(df, gw[k]));
-      den[k] = __dadd_rn(den[k], __dmul_rn(-dx[k], gw[k]));
-      scale[k] = __dadd_rn(scale[k], fabs(__dmul_rn(dx[k], gw[k])));
+      t.num[k] = __dmul_rn(df, gw[k]);
+      t.den[k] = __dmul_rn(-dx[k], gw[k]);
+      t.scale[k] = fabs(__dmul_rn(dx[k], gw[k]));
+    }
+    return t;
+  }
+  __device__ __forceinline__ void acc(const W2Term& t) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      num[k] = __dadd_rn(num[k], t.num[k]);
+      den[k] = __dadd_rn(den[k], t.den[k]);
+      scale[k] = __dadd_rn(scale[k], t.scale[k]);
     }
   }
+  __device__ __forceinline__ void add(const Win2Args& a, int j) { acc(term(a, j)); }
   // g_k = num/den, or 0 and a degenerate count (gradient.cpp:73-80)
   __device__ __forceinline__ unsigned long long finish(const Win2Args& a, int i) const {
     unsigned long long deg = 0;
@@ -971,9 +987,16 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
 #pragma unroll
       for (int kk = 0; kk < 2; ++kk) acc.xi[kk] = __ldg(a.gx[kk] + i);
       acc.fi = __ldg(a.gf + i);
-      if (fits) {  // the thread's own sorted row
+      acc.ih = __drcp_rn(a.gh);
+      if (fits) {  // the thread's own sorted row, two neighbours' terms in flight
         const SharedRow row{sa(S.pk) + 4u * (uint32_t)excl};
-        for (int e = 0; e < k; ++e) acc.add(a, row.ld(e));
+        int e = 0;
+        for (; e + 1 < k; e += 2) {
+          const W2Term t0 = acc.term(a, row.ld(e)), t1 = acc.term(a, row.ld(e + 1));
+          acc.acc(t0);
+          acc.acc(t1);
+        }
+        if (e < k) acc.add(a, row.ld(e));
       } else {
         w2_slow_grad(a, i, cx, cy, rxh, ryh, acc);
       }
