@@ -22,6 +22,8 @@ order = np.lexsort((np.arange(n), cell))        # CSR order: cell, then id
 starts = np.searchsorted(cell[order], np.arange(nc ** 3 + 1))
 rng = np.random.default_rng(0)
 warps = rng.choice(n // 32, 400, replace=False)
+GS = int(sys.argv[1]) if len(sys.argv) > 1 else 32   # records per group
+AX = sys.argv[2] if len(sys.argv) > 2 else "yz"       # axes of the bounding box
 tot = lane_skip = warp_skip = 0
 for w in warps:
     lanes = order[32 * w: 32 * w + 32]
@@ -41,17 +43,19 @@ for w in warps:
                         q = (z * nc + yy) * nc + xx
                         mem.append(order[starts[q]:starts[q + 1]])
             run = np.sort(np.concatenate(mem))          # id-merged run
-            for g in range(0, len(run), 32):
-                grp = run[g:g + 32]
-                # per lane: minimum possible distance to the group's (y, z) box
-                ylo, yhi = x[1][grp].min(), x[1][grp].max()
-                zlo, zhi = x[2][grp].min(), x[2][grp].max()
-                gy = np.maximum(0, np.maximum(ylo - x[1][L], x[1][L] - yhi))
-                gz = np.maximum(0, np.maximum(zlo - x[2][L], x[2][L] - zhi))
-                skip = gy ** 2 + gz ** 2 >= cut ** 2
+            for g in range(0, len(run), GS):
+                grp = run[g:g + GS]
+                # per lane: minimum possible distance to the group's bounding box
+                d2 = 0.0
+                for k in range(3):
+                    if "xyz"[k] not in AX:
+                        continue
+                    lo, hi = x[k][grp].min(), x[k][grp].max()
+                    d2 = d2 + np.maximum(0, np.maximum(lo - x[k][L], x[k][L] - hi)) ** 2
+                skip = d2 >= cut ** 2
                 tot += len(L)
                 lane_skip += skip.sum()
                 # the warp runs this cell's lanes' loop together with the other cells' lanes
                 warp_skip += len(L) if skip.all() else 0
-print(f"C3 groups x lanes {tot}: per-lane skippable {lane_skip / tot:.1%}, "
+print(f"group {GS} box {AX}: C3 groups x lanes {tot}: per-lane skippable {lane_skip / tot:.1%}, "
       f"warp-uniform skippable {warp_skip / tot:.1%}")
