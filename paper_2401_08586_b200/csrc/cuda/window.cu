@@ -80,11 +80,11 @@ static_assert(sizeof(W2Desc) % 16 == 0, "bulk-copied");
 
 template <int BT>
 struct W2Cfg {
-  static constexpr int WCap = 12 * BT + BT / 2;  // window records
-  static constexpr int PCap = WCap * 3 / 2;      // packed row entries (alias the coordinates)
-  static constexpr int CSCap = 4 * BT;           // window cell boundaries
+  static constexpr int WCap = 12 * BT + BT / 4;  // window records
+  static constexpr int PCap = WCap * 3 / 2 + 48;  // packed row entries (alias the coordinates)
+  static constexpr int CSCap = 3 * BT;            // window cell boundaries
   static constexpr int RunCap = 7 * BT / 4;      // run lists
-  static constexpr int MinB = 1024 / BT;         // CTAs per SM (register budget)
+  static constexpr int MinB = BT == 128 ? 9 : 4;  // CTAs per SM (register budget: <= 56 at 9)
 };
 
 __device__ __forceinline__ unsigned h2u(__half2 h) { return *reinterpret_cast<const unsigned*>(&h); }
@@ -244,12 +244,12 @@ struct W2Smem {
   int id[C::WCap];                 // candidate particle ids
   uint4 run[C::RunCap * 2];        // run lists of the window's centre cells (32 bytes each)
   short cs[C::CSCap];              // window cell boundaries, relative to the row's CSR start
-  unsigned hw[3][BT];              // phase A hit words of the 3 segments
   W2Desc d;                        // the tile's bands and window rows (from the pack)
   int wsum[BT / 32];
   long long base;
   unsigned long long bar;
 };
+static_assert(sizeof(W2Smem<128>::pk) <= sizeof(W2Smem<128>::c), "packed rows alias the coordinates");
 
 // Where a segment's records are read from: the staged window (shared memory,
 // window positions) or the pack's CSR-order arrays (global memory, CSR
@@ -747,7 +747,7 @@ __device__ void w2_slow_grad(const Win2Args& a, int i, int cxi, int cyi, __half 
 // GRAD: the fused NNPS -> grad_normalized (no table): each packed row is walked
 // in id order into the FP64 sums of its particle.
 template <int BT, bool GRAD>
-__global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
+__global__ void __launch_bounds__(BT, GRAD ? 1024 / BT : W2Cfg<BT>::MinB) k_w2(Win2Args a) {
   using Cfg = W2Cfg<BT>;
   extern __shared__ __align__(128) unsigned char smraw[];
   W2Smem<BT>& S = *reinterpret_cast<W2Smem<BT>*>(smraw);
@@ -869,6 +869,7 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
     return g;
   };
   const int selfcsr = valid ? __ldg(a.wself + i) : 0;
+  unsigned hw[3];  // phase A hit words of the 3 segments (registers: s is unrolled there)
   auto phase_a = [&](const auto& src) {  // every lane: warp-uniform loops
     int tot = 0;
 #pragma unroll
@@ -905,7 +906,7 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
         if (sp >= g.pC && sp < g.pR) H &= ~(1u << (sp - p0));
         else slow = true;  // RelCoords cell is not the CSR cell (a stale grid)
       }
-      S.hw[s][tid] = H;
+      hw[s] = H;
       tot += __popc(H);
     }
     k = tot;
@@ -934,7 +935,7 @@ __global__ void __launch_bounds__(BT, W2Cfg<BT>::MinB) k_w2(Win2Args a) {
     int kk = 0;
 #pragma unroll 1
     for (int s = 0; s < 3; ++s) {
-      const unsigned H = part ? S.hw[s][tid] : 0u;
+      const unsigned H = part ? (s == 0 ? hw[0] : (s == 1 ? hw[1] : hw[2])) : 0u;
       Seg g{0, 0, 0, 0, -1};
       if (H) g = seg(s);
       const int pL = g.pL, len = g.pE - g.pL;
