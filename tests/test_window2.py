@@ -161,3 +161,21 @@ def test_matches_encode_path(ctx):
     b = ctx.rcll(g, rel, cell, items, start, 2)
     os.environ["SPHX_W2"] = "1"
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("nx_cells", [2048, 2200])
+def test_wide_grids(ctx, nx_cells):
+    """A strip domain at and past the windowed path's 2048-cell row limit (past it
+    the rows go to the encode path): the table equals the oracle's either way."""
+    import paper_2401_08586_b200 as P
+    orc = O.Oracle()
+    ds = 0.002
+    radius = 2.4 * ds
+    hi = (nx_cells * radius - 1e-9, 12 * ds, 1.0)
+    x = orc.lattice(2, ds, 0.3, 11, (0, 0, 0), hi)
+    g = P.grid_init(2, (0, 0, 0), hi, radius)
+    assert g.counts[0] == nx_cells
+    (off, it), (rel, cell, items, start) = _table(ctx, P, g, x)
+    og = orc.grid(2, radius, (0, 0, 0), hi)
+    want = orc.rcll(og, rel, cell, items, start, O.FP16)
+    assert np.array_equal(off, want.offsets) and np.array_equal(it, want.items)
