@@ -674,11 +674,19 @@ struct W2Term {
 struct W2Grad {
   double num[2] = {0.0, 0.0}, den[2] = {0.0, 0.0}, scale[2] = {0.0, 0.0};
   double xi[2], fi, ih;  // ih = RN(1/h)
-  __device__ __forceinline__ W2Term term(const Win2Args& a, int j) const {
+  // neighbour j's inputs (positions, field value)
+  struct Nb {
+    double x[2], f;
+  };
+  __device__ __forceinline__ static Nb load(const Win2Args& a, int j) {
+    return Nb{{__ldg(a.gx[0] + j), __ldg(a.gx[1] + j)}, __ldg(a.gf + j)};
+  }
+  __device__ __forceinline__ W2Term term(const Win2Args& a, int j) const { return term(a, load(a, j)); }
+  __device__ __forceinline__ W2Term term(const Win2Args& a, const Nb& nb) const {
     double dx[2], gw[2] = {0.0, 0.0}, r2 = 0.0;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      dx[k] = __dsub_rn(xi[k], __ldg(a.gx[k] + j));
+      dx[k] = __dsub_rn(xi[k], nb.x[k]);
       r2 = __dadd_rn(r2, __dmul_rn(dx[k], dx[k]));
     }
     const double r = __dsqrt_rn(r2);
@@ -688,7 +696,7 @@ struct W2Grad {
 #pragma unroll
       for (int k = 0; k < 2; ++k) gw[k] = __dmul_rn(sc, dx[k]);
     }
-    const double df = __dsub_rn(__ldg(a.gf + j), fi);
+    const double df = __dsub_rn(nb.f, fi);
     W2Term t;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
@@ -989,16 +997,16 @@ __global__ void __launch_bounds__(BT, GRAD ? 1024 / BT : W2Cfg<BT>::MinB) k_w2(W
       for (int kk = 0; kk < 2; ++kk) acc.xi[kk] = __ldg(a.gx[kk] + i);
       acc.fi = __ldg(a.gf + i);
       acc.ih = __drcp_rn(a.gh);
-      if (fits) {  // the thread's own sorted row, two neighbours' terms in flight
+      if (fits && k > 0) {  // the thread's own sorted row; the next neighbour's
+                            // inputs are loaded while this one's term is computed
         const SharedRow row{sa(S.pk) + 4u * (uint32_t)excl};
-        int e = 0;
-        for (; e + 1 < k; e += 2) {
-          const W2Term t0 = acc.term(a, row.ld(e)), t1 = acc.term(a, row.ld(e + 1));
-          acc.acc(t0);
-          acc.acc(t1);
+        W2Grad::Nb cur = W2Grad::load(a, row.ld(0));
+        for (int e = 0; e < k; ++e) {
+          const W2Grad::Nb nxt = W2Grad::load(a, row.ld(e + 1 < k ? e + 1 : e));
+          acc.acc(acc.term(a, cur));
+          cur = nxt;
         }
-        if (e < k) acc.add(a, row.ld(e));
-      } else {
+      } else if (!fits) {
         w2_slow_grad(a, i, cx, cy, rxh, ryh, acc);
       }
       deg = acc.finish(a, i);
