@@ -1278,11 +1278,24 @@ template <int D>
 struct GradAcc {
   double num[3] = {0.0, 0.0, 0.0}, den[3] = {0.0, 0.0, 0.0}, scale[3] = {0.0, 0.0, 0.0};
   double xi[3], fi, ih;  // ih = RN(1/h)
+  struct Nb {  // neighbour j's inputs (positions, field value)
+    double x[3], f;
+  };
+  __device__ __forceinline__ static Nb load(const SweepArgs& a, int j) {
+    Nb nb;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) nb.x[k] = k < D ? __ldg(a.gx[k] + j) : 0.0;
+    nb.f = __ldg(a.gf + j);
+    return nb;
+  }
   __device__ __forceinline__ GradTerm<D> term(const SweepArgs& a, int j) const {
+    return term(a, load(a, j));
+  }
+  __device__ __forceinline__ GradTerm<D> term(const SweepArgs& a, const Nb& nb) const {
     double dx[3], gw[3] = {0.0, 0.0, 0.0}, r2 = 0.0;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      dx[k] = __dsub_rn(xi[k], __ldg(a.gx[k] + j));
+      dx[k] = __dsub_rn(xi[k], nb.x[k]);
       r2 = __dadd_rn(r2, __dmul_rn(dx[k], dx[k]));
     }
     const double r = __dsqrt_rn(r2);
@@ -1292,7 +1305,7 @@ struct GradAcc {
 #pragma unroll
       for (int k = 0; k < D; ++k) gw[k] = __dmul_rn(sc, dx[k]);
     }
-    const double df = __dsub_rn(__ldg(a.gf + j), fi);
+    const double df = __dsub_rn(nb.f, fi);
     GradTerm<D> t;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
@@ -1371,13 +1384,14 @@ __global__ void __launch_bounds__(BT) k_r16_grad(SweepArgs a) {
         }
         if (gs > 0 && kk > gs && row.ld(gs) < row.ld(gs - 1)) merge_tail(row, gs, kk);
       });
-      int e = 0;  // two neighbours' terms in flight, summed in row order
-      for (; e + 1 < k; e += 2) {
-        const GradTerm<D> t0 = acc.term(a, row.ld(e)), t1 = acc.term(a, row.ld(e + 1));
-        acc.acc(t0);
-        acc.acc(t1);
+      if (k > 0) {  // the next neighbour's inputs load while this term is computed
+        typename GradAcc<D>::Nb cur = GradAcc<D>::load(a, row.ld(0));
+        for (int e = 0; e < k; ++e) {
+          const typename GradAcc<D>::Nb nxt = GradAcc<D>::load(a, row.ld(e + 1 < k ? e + 1 : e));
+          acc.acc(acc.term(a, cur));
+          cur = nxt;
+        }
       }
-      if (e < k) acc.add(a, row.ld(e));
     } else {
       // long row: ids in ascending order by repeated minimum search over the hits
       int last = INT_MIN;
