@@ -63,7 +63,7 @@ namespace {
 constexpr int kSegMax = 32;   // positions per segment (one hit word, one run list)
 constexpr int kRowsMax = 12;  // window rows (both bands)
 constexpr int kBandRows = 6;  // rows of one band: ymax - ymin <= 3
-constexpr int kPackR = 4;     // records per pack thread
+constexpr int kPackR = 2;     // records per pack thread
 
 // A tile's window, computed by the pack (one warp per tile) and brought into
 // the sweep's shared memory with one bulk copy. fast = 0: no window (the tile's
