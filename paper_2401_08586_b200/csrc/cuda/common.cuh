@@ -141,7 +141,7 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
   return v;
 }
 
-__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
@@ -169,10 +169,10 @@ __device__ __forceinline__ long long lookback_exclusive(unsigned long long* tile
   const unsigned long long AGG = 1ull << 62, PRE = 2ull << 62, VAL = (1ull << 62) - 1;
   const int lane = threadIdx.x & 31;
   if (bid == 0) {
-    if (lane == 0) st_release_u64(&tiles[0], PRE | (unsigned long long)block_total);
+    if (lane == 0) st_relaxed_u64(&tiles[0], PRE | (unsigned long long)block_total);
     return 0;
   }
-  if (lane == 0) st_release_u64(&tiles[bid], AGG | (unsigned long long)block_total);
+  if (lane == 0) st_relaxed_u64(&tiles[bid], AGG | (unsigned long long)block_total);
   long long excl = 0;
   int p = bid - 1;
   unsigned backoff = 32;
@@ -196,7 +196,7 @@ __device__ __forceinline__ long long lookback_exclusive(unsigned long long* tile
     if (first < 32) break;
     p -= 32;
   }
-  if (lane == 0) st_release_u64(&tiles[bid], PRE | (unsigned long long)(excl + block_total));
+  if (lane == 0) st_relaxed_u64(&tiles[bid], PRE | (unsigned long long)(excl + block_total));
   return excl;
 }
 

@@ -686,7 +686,7 @@ __device__ __forceinline__ void stream_tile(int32_t* gout, const SharedRow& pk, 
 __device__ __forceinline__ void lookback_publish(unsigned long long* tiles, int bid, long long total,
                                                  unsigned epoch) {
   const unsigned long long E = (unsigned long long)epoch << 48;
-  st_release_u64(&tiles[bid], E | ((bid == 0 ? 2ull : 1ull) << 46) | (unsigned long long)total);
+  st_relaxed_u64(&tiles[bid], E | ((bid == 0 ? 2ull : 1ull) << 46) | (unsigned long long)total);
 }
 
 __device__ __forceinline__ long long lookback_resolve(unsigned long long* tiles, int bid,
@@ -719,7 +719,7 @@ __device__ __forceinline__ long long lookback_resolve(unsigned long long* tiles,
     if (first < 32) break;
     p -= 32;
   }
-  if (lane == 0) st_release_u64(&tiles[bid], E | PRE | (unsigned long long)(excl + total));
+  if (lane == 0) st_relaxed_u64(&tiles[bid], E | PRE | (unsigned long long)(excl + total));
   return excl;
 }
 

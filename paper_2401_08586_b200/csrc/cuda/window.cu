@@ -64,6 +64,10 @@ constexpr int kSegMax = 32;   // positions per segment (one hit word, one run li
 constexpr int kRowsMax = 12;  // window rows (both bands)
 constexpr int kBandRows = 6;  // rows of one band: ymax - ymin <= 3
 constexpr int kPackR = 2;     // records per pack thread
+#ifndef SPHX_EXP
+#define SPHX_EXP 0
+#endif
+constexpr int kExp = SPHX_EXP;  // A/B experiment bits (tools/exp_build.sh); 0 = the default build
 
 // A tile's window, computed by the pack (one warp per tile) and brought into
 // the sweep's shared memory with one bulk copy. fast = 0: no window (the tile's
@@ -158,7 +162,7 @@ __device__ __forceinline__ void insertion_sort(const Row& dst, int k) {
 __device__ __forceinline__ void lb_publish(unsigned long long* tiles, int bid, long long total,
                                            unsigned epoch) {
   const unsigned long long E = (unsigned long long)epoch << 48;
-  st_release_u64(&tiles[bid], E | ((bid == 0 ? 2ull : 1ull) << 46) | (unsigned long long)total);
+  st_relaxed_u64(&tiles[bid], E | ((bid == 0 ? 2ull : 1ull) << 46) | (unsigned long long)total);
 }
 
 __device__ __forceinline__ long long lb_resolve(unsigned long long* tiles, int bid, long long total,
@@ -191,7 +195,7 @@ __device__ __forceinline__ long long lb_resolve(unsigned long long* tiles, int b
     if (first < 32) break;
     p -= 32;
   }
-  if (lane == 0) st_release_u64(&tiles[bid], E | PRE | (unsigned long long)(excl + total));
+  if (lane == 0) st_relaxed_u64(&tiles[bid], E | PRE | (unsigned long long)(excl + total));
   return excl;
 }
 
@@ -244,7 +248,7 @@ struct W2Smem {
   int id[C::WCap];                 // candidate particle ids
   uint4 run[C::RunCap * 2];        // run lists of the window's centre cells (32 bytes each)
   short cs[C::CSCap];              // window cell boundaries, relative to the row's CSR start
-  W2Desc d;                        // the tile's bands and window rows (from the pack)
+  alignas(16) W2Desc d;            // the tile's bands and window rows (from the pack)
   int wsum[BT / 32];
   long long base;
   unsigned long long bar;
@@ -779,6 +783,48 @@ __global__ void __launch_bounds__(BT, GRAD ? 1024 / BT : W2Cfg<BT>::MinB) k_w2(W
   const __half rxh = __double2half(__ldg(a.rel[0] + i));
   const __half ryh = __double2half(__ldg(a.rel[1] + i));
 
+  // one warp polls the barrier (phase `ph`); the others wait at __syncthreads
+  auto wait_bar = [&](unsigned ph) {
+    if (warp == 0)
+      asm volatile(
+          "{\n\t.reg .pred P;\n"
+          "W2WAIT%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+          "@!P bra W2WAIT%=;\n\t}" ::"r"(bar),
+          "r"(ph)
+          : "memory");
+    __syncthreads();
+  };
+  // warp 0: stage the window (TMA bulk copies) -- one lane per window row issues
+  // its row's copies after lane 0 has armed the barrier with the window's bytes
+  auto issue_window = [&](const Geo& G, int nrw) {
+    const int rr = lane;
+    const int gy = rr < nrw ? S.d.rgy[rr] : -1;
+    const int q = rr < G.rows[0] ? 0 : 1;
+    const unsigned rb = gy >= 0 ? 32u * (unsigned)G.nrun_of(q) : 0u;
+    const unsigned tx = (unsigned)S.d.total * 10u + __reduce_add_sync(0xffffffffu, rb);
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx)
+                   : "memory");
+    __syncwarp();
+    if (gy >= 0) {
+      const int n8 = S.d.rn[rr], a8 = S.d.ra8[rr], wb = S.d.rbase[rr];
+      const void* src[4] = {a.wxy + 2 * (int64_t)a8, a.wu + a8, a.wid + a8,
+                            a.wrun + ((int64_t)gy * nx + S.d.bx[q][0]) * kSegMax};
+      const uint32_t dst[4] = {sa(&S.c.xy[wb >> 1]), sa(&S.c.u[wb]), sa(&S.id[wb]),
+                               sa(&S.run[2 * G.run0(rr)])};
+      const unsigned bytes[4] = {4u * n8, 2u * n8, 4u * n8, rb};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (bytes[c] == 0) continue;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                dst[c]),
+            "l"(src[c]), "r"(bytes[c]), "r"(bar)
+            : "memory");
+      }
+    }
+  };
   // ---- the tile's descriptor (bands, window rows: the pack's tile warps) ----
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
@@ -793,54 +839,16 @@ __global__ void __launch_bounds__(BT, GRAD ? 1024 / BT : W2Cfg<BT>::MinB) k_w2(W
         "l"(static_cast<const W2Desc*>(a.desc) + tile), "r"((unsigned)sizeof(W2Desc)), "r"(bar)
         : "memory");
   }
-  // one warp polls the barrier (phase `ph`); the others wait at __syncthreads
-  auto wait_bar = [&](unsigned ph) {
-    if (warp == 0)
-      asm volatile(
-          "{\n\t.reg .pred P;\n"
-          "W2WAIT%=:\n\t"
-          "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
-          "@!P bra W2WAIT%=;\n\t}" ::"r"(bar),
-          "r"(ph)
-          : "memory");
-    __syncthreads();
-  };
   wait_bar(0);
   bool fast = S.d.fast;
   const int b = (S.d.nb == 2 && tid >= S.d.split) ? 1 : 0;
   const Geo G = geo_of(S.d.bx, fast ? S.d.nb : 0);
   const int nrw = G.rows[0] + G.rows[1];
 
-  // ---- stage the window (TMA bulk copies) while the warps fill the cell
-  // boundaries (cell_start is an input): a warp per row ----
+  // ---- the window's cell boundaries (cell_start is an input) while the copies
+  // fly: a warp per row ----
   if (fast) {
-    if (tid == 0) {
-      unsigned tx = (unsigned)S.d.total * 10u;
-      for (int rr = 0; rr < nrw; ++rr)
-        if (S.d.rgy[rr] >= 0) tx += 32u * (unsigned)G.nrun_of(rr < G.rows[0] ? 0 : 1);
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx)
-                   : "memory");
-      for (int rr = 0; rr < nrw; ++rr) {
-        const int gy = S.d.rgy[rr];
-        if (gy < 0) continue;
-        const int q = rr < G.rows[0] ? 0 : 1;
-        const int n8 = S.d.rn[rr], a8 = S.d.ra8[rr], wb = S.d.rbase[rr];
-        const void* src[4] = {a.wxy + 2 * (int64_t)a8, a.wu + a8, a.wid + a8,
-                              a.wrun + ((int64_t)gy * nx + S.d.bx[q][0]) * kSegMax};
-        const uint32_t dst[4] = {sa(&S.c.xy[wb >> 1]), sa(&S.c.u[wb]), sa(&S.id[wb]),
-                                 sa(&S.run[2 * G.run0(rr)])};
-        const unsigned bytes[4] = {4u * n8, 2u * n8, 4u * n8, 32u * (unsigned)G.nrun_of(q)};
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (bytes[c] == 0) continue;
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  dst[c]),
-              "l"(src[c]), "r"(bytes[c]), "r"(bar)
-              : "memory");
-        }
-      }
-    }
+    if (warp == 0) issue_window(G, nrw);
     for (int rr = warp; rr < nrw; rr += BT / 32) {
       const int q = rr < G.rows[0] ? 0 : 1;
       const int ncs = G.ncs_of(q), cs0 = G.cs0(rr);
