@@ -532,7 +532,7 @@ def run_ours(args):
             rp = [t.data_ptr() for t in h_rel]
             cp = [t.data_ptr() for t in h_cell]
             for _ in range(2):
-                ctx.rcll_ptr(grid, n, rp, cp, h_items.data_ptr(), h_start.data_ptr(), prec)
+                tot = ctx.rcll_ptr(grid, n, rp, cp, h_items.data_ptr(), h_start.data_ptr(), prec)
                 ctx.table_copy_ptr(h_off.data_ptr(), h_out.data_ptr())
             for _ in range(args.e2e_steps):
                 t0 = time.perf_counter()
