@@ -22,7 +22,8 @@
 //               ymin-1 .. ymax+1, cells xmin-1 .. xmax+1 -- is one contiguous CSR
 //               range per cell row (linear cell = cx + nx*cy, x fastest,
 //               cell_grid.hpp:74-78), staged in shared memory with TMA bulk
-//               copies (cp.async.bulk, one mbarrier) together with the run lists
+//               copies (cp.async.bulk, one mbarrier, one lane of warp 0 per window
+//               row issuing that row's copies) together with the run lists
 //               of its centre cells. A target's candidates in stencil row oy are
 //               one contiguous window segment (cells cx-1, cx, cx+1):
 //               A  tested two per binary16x2 op straight from shared memory
@@ -64,10 +65,6 @@ constexpr int kSegMax = 32;   // positions per segment (one hit word, one run li
 constexpr int kRowsMax = 12;  // window rows (both bands)
 constexpr int kBandRows = 6;  // rows of one band: ymax - ymin <= 3
 constexpr int kPackR = 2;     // records per pack thread
-#ifndef SPHX_EXP
-#define SPHX_EXP 0
-#endif
-constexpr int kExp = SPHX_EXP;  // A/B experiment bits (tools/exp_build.sh); 0 = the default build
 
 // A tile's window, computed by the pack (one warp per tile) and brought into
 // the sweep's shared memory with one bulk copy. fast = 0: no window (the tile's
