@@ -251,30 +251,28 @@ struct W2Smem {
   unsigned long long bar;
 };
 static_assert(sizeof(W2Smem<128>::pk) <= sizeof(W2Smem<128>::c), "packed rows alias the coordinates");
+static_assert(W2Cfg<256>::WCap < (1 << 12) && W2Cfg<256>::RunCap < (1 << 14) && kSegMax < (1 << 6),
+              "segment words: window position 12 bits, length 6 bits, run list 14 bits");
 
 // Where a segment's records are read from: the staged window (shared memory,
 // window positions) or the pack's CSR-order arrays (global memory, CSR
 // positions; tiles without a window). Positions keep their parity in both, so
 // pair p/2 is the same record pair.
 struct SmemSrc {  // 32-bit shared addresses of the window's arrays
-  static constexpr int kAlign = 2;  // positions per pair load
+  // a segment's first pair load starts at a multiple of 4 positions, so a group of
+  // 4 pairs is two 16-byte loads of coordinates and two 8-byte loads of cell x
+  static constexpr int kAlign = 4;
   uint32_t xy, u, id;
   __device__ __forceinline__ void quad(int q, uint2 (&v)[4], unsigned (&w)[4]) const {
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      v[t] = pair(q + t);
-      w[t] = upair(q + t);
+    for (int h = 0; h < 2; ++h) {
+      asm("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+          : "=r"(v[2 * h].x), "=r"(v[2 * h].y), "=r"(v[2 * h + 1].x), "=r"(v[2 * h + 1].y)
+          : "r"(xy + 8u * (uint32_t)(q + 2 * h)));
+      asm("ld.shared.v2.b32 {%0, %1}, [%2];"
+          : "=r"(w[2 * h]), "=r"(w[2 * h + 1])
+          : "r"(u + 4u * (uint32_t)(q + 2 * h)));
     }
-  }
-  __device__ __forceinline__ uint2 pair(int q) const {
-    uint2 v;
-    asm("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(xy + 8u * (uint32_t)q));
-    return v;
-  }
-  __device__ __forceinline__ unsigned upair(int q) const {
-    unsigned v;
-    asm("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(u + 4u * (uint32_t)q));
-    return v;
   }
   __device__ __forceinline__ int ident(int p) const {
     int v;
@@ -883,6 +881,9 @@ __global__ void __launch_bounds__(BT, GRAD ? 1024 / BT : W2Cfg<BT>::MinB) k_w2(W
   };
   const int selfcsr = valid ? __ldg(a.wself + i) : 0;
   unsigned hw[3];  // phase A hit words of the 3 segments (registers: s is unrolled there)
+  // window tiles: each segment's start, length and run-list slot, packed by phase A
+  // (pL | len << 12 | run << 18) so that phase B does not derive them again
+  unsigned sg[3] = {0u, 0u, 0u};
   auto phase_a = [&](const auto& src) {  // every lane: warp-uniform loops
     int tot = 0;
 #pragma unroll
@@ -920,6 +921,9 @@ __global__ void __launch_bounds__(BT, GRAD ? 1024 / BT : W2Cfg<BT>::MinB) k_w2(W
         else slow = true;  // RelCoords cell is not the CSR cell (a stale grid)
       }
       hw[s] = H;
+      if constexpr (std::is_same_v<std::decay_t<decltype(src)>, SmemSrc>)
+        sg[s] = (unsigned)g.pL | ((unsigned)(g.pE - g.pL) << 12) |
+                ((unsigned)(G.run0(g.r) + cx - S.d.bx[b][0]) << 18);
       tot += __popc(H);
     }
     k = tot;
@@ -949,16 +953,21 @@ __global__ void __launch_bounds__(BT, GRAD ? 1024 / BT : W2Cfg<BT>::MinB) k_w2(W
 #pragma unroll 1
     for (int s = 0; s < 3; ++s) {
       const unsigned H = part ? (s == 0 ? hw[0] : (s == 1 ? hw[1] : hw[2])) : 0u;
+      constexpr bool kSg = std::is_same_v<std::decay_t<decltype(src)>, SmemSrc>;
       Seg g{0, 0, 0, 0, -1};
-      if (H) g = seg(s);
-      const int pL = g.pL, len = g.pE - g.pL;
+      unsigned sgw = 0;
+      if constexpr (kSg) sgw = H ? (s == 0 ? sg[0] : (s == 1 ? sg[1] : sg[2])) : 0u;
+      else if (H) g = seg(s);
+      const int pL = kSg ? (int)(sgw & 0xFFFu) : g.pL;
+      const int len = kSg ? (int)((sgw >> 12) & 0x3Fu) : g.pE - g.pL;
       const int lmax = __reduce_max_sync(0xffffffffu, len);
       if (lmax == 0) continue;
       constexpr int kA = std::decay_t<decltype(src)>::kAlign;
       const unsigned hrel = H >> (pL & (kA - 1));  // bit o = position pL + o
       uint4 w[2];
       if (fast) {
-        const uint4* rl = &S.run[2 * (H ? G.run0(g.r) + cx - S.d.bx[b][0] : 0)];
+        const uint4* rl =
+            kSg ? &S.run[2 * (sgw >> 18)] : &S.run[2 * (H ? G.run0(g.r) + cx - S.d.bx[b][0] : 0)];
         w[0] = rl[0];
         w[1] = rl[1];
       } else {
@@ -967,18 +976,45 @@ __global__ void __launch_bounds__(BT, GRAD ? 1024 / BT : W2Cfg<BT>::MinB) k_w2(W
         w[1] = __ldg(rl + 1);
       }
       const int gs = kk;
+      if constexpr (std::is_same_v<std::decay_t<decltype(src)>, SmemSrc> &&
+                    std::is_same_v<std::decay_t<decltype(dst)>, SharedRow>) {
+        // shared addresses carried in bytes: the segment's ids from idb, the row's
+        // next slot at da (advanced by 4 per hit); one PRMT per run-list offset
+        const uint32_t idb = src.id + 4u * (uint32_t)pL;
+        uint32_t da = dst.base + 4u * (uint32_t)kk;
 #pragma unroll
-      for (int t4 = 0; t4 < 8; ++t4) {
-        if (4 * t4 >= lmax) break;
-        const unsigned word = t4 < 4 ? (&w[0].x)[t4] : (&w[1].x)[t4 - 4];
+        for (int t4 = 0; t4 < 8; ++t4) {
+          if (4 * t4 >= lmax) break;
+          const unsigned word = t4 < 4 ? (&w[0].x)[t4] : (&w[1].x)[t4 - 4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const unsigned off = (word >> (8 * u)) & 0xFFu;  // 0xFF past the run
-          unsigned sh;
-          asm("shr.b32 %0, %1, %2;" : "=r"(sh) : "r"(hrel), "r"(off));  // (0 for off >= 32)
-          const bool hit = sh & 1u;
-          if (hit) dst.st(kk, src.ident(pL + (int)off));
-          kk += hit;
+          for (int u = 0; u < 4; ++u) {
+            const unsigned off = __byte_perm(word, 0u, 0x4440u | u);  // 0xFF past the run
+            unsigned sh;
+            asm("shr.b32 %0, %1, %2;" : "=r"(sh) : "r"(hrel), "r"(off));  // (0 for off >= 32)
+            const unsigned hit = sh & 1u;
+            if (hit) {
+              int v;
+              asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(idb + 4u * off) : "memory");
+              asm volatile("st.shared.b32 [%0], %1;" ::"r"(da), "r"(v) : "memory");
+            }
+            da += hit << 2;
+          }
+        }
+        kk = (int)((da - dst.base) >> 2);
+      } else {
+#pragma unroll
+        for (int t4 = 0; t4 < 8; ++t4) {
+          if (4 * t4 >= lmax) break;
+          const unsigned word = t4 < 4 ? (&w[0].x)[t4] : (&w[1].x)[t4 - 4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const unsigned off = (word >> (8 * u)) & 0xFFu;  // 0xFF past the run
+            unsigned sh;
+            asm("shr.b32 %0, %1, %2;" : "=r"(sh) : "r"(hrel), "r"(off));  // (0 for off >= 32)
+            const bool hit = sh & 1u;
+            if (hit) dst.st(kk, src.ident(pL + (int)off));
+            kk += hit;
+          }
         }
       }
       if (gs > 0 && kk > gs && dst.ld(gs) < dst.ld(gs - 1)) merge_tail(dst, gs, kk);
